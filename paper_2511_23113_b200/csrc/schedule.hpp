@@ -1,0 +1,56 @@
+// Work schedule of the block-sparse attention kernel.
+//
+// One work item = one local head x one 128-row Q tile (two 64-row Q blocks of
+// the same head, or one block padded to 128 rows).  Its entries are the KV
+// blocks in the union of the two rows' dense sets, each tagged with which
+// half actually needs it.  tcgen05 runs M=128 tiles at the same issue cost as
+// M=64 (B300_MICROARCH.md: floor = max(M,128)*N/256 cycles), so pairing two
+// 64-row Q blocks is never slower than one M=64 tile per block and is twice
+// as fast when their KV sets coincide.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "core.hpp"
+
+namespace dbsp_core {
+
+// Device layout: 32 bytes, read once per CTA.
+struct alignas(16) WorkItem {
+  uint32_t head;    // local head index in the Q/K/V buffers
+  uint32_t qa;      // local Q block of rows 0..63
+  uint32_t qb;      // local Q block of rows 64..127 (== qa when single)
+  uint32_t begin;   // first entry
+  uint32_t count;   // entries (KV tiles visited)
+  uint32_t single;  // 1: rows 64..127 are padding
+  uint32_t pad0, pad1;
+};
+
+// Entry bit layout.
+constexpr uint32_t kEntryKvMask = (1u << 22) - 1;  // local KV block index
+constexpr uint32_t kEntryDenseA = 1u << 22;        // tile dense for rows 0..63
+constexpr uint32_t kEntryDenseB = 1u << 23;        // tile dense for rows 64..127
+constexpr uint32_t kEntryValidShift = 24;          // (valid keys - 1), 6 bits
+
+struct LocalView {
+  uint32_t heads = 0, q_blocks = 0, kv_blocks = 0;
+  const uint32_t* head_ids = nullptr;  // null = identity
+  const uint32_t* q_ids = nullptr;
+  const uint32_t* kv_ids = nullptr;
+  uint32_t kv_tokens_global = 0;  // 0 = every block full
+};
+
+struct Schedule {
+  std::vector<WorkItem> items;
+  std::vector<uint32_t> entries;
+  uint64_t tile_visits = 0;  // sum of counts (MMA tiles issued)
+  uint64_t dense_tiles = 0;  // 64x64 tiles actually dense (softmax work)
+};
+
+// Builds items ordered by local head, heaviest first within a head (keeps
+// the K/V working set of concurrently running CTAs L2-resident while the
+// heaviest tiles start first).
+void build_schedule(const MaskView& m, const LocalView& v, bool pair_q, Schedule& out);
+
+}  // namespace dbsp_core

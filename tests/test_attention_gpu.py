@@ -1,0 +1,153 @@
+"""GPU parity of the sm_100a block-sparse attention kernel (K4) against the CPU
+oracle (oracle/attention_ref.c, fp32 inputs, double accumulation).
+
+Tolerance (north_star): bf16 output within max-abs 2e-2 and rel-L2 1e-2 of the
+oracle.  Inputs are the bf16-rounded Q/K/V, so the comparison measures the
+kernel's arithmetic, not input quantisation.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # test infrastructure: the checker
+import paper_2511_23113_b200 as D
+from paper_2511_23113_b200.attention import AttentionSchedule, accum_init, sparse_attention
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-2
+REL_L2 = 1e-2
+
+
+def make_qkv(S, H, d, seed, Sk=None):
+    g = torch.Generator().manual_seed(seed)
+    Sk = Sk or S
+    q = torch.randn(S, H, d, generator=g).to(torch.bfloat16)
+    k = torch.randn(Sk, H, d, generator=g).to(torch.bfloat16)
+    v = torch.randn(Sk, H, d, generator=g).to(torch.bfloat16)
+    return q, k, v
+
+
+def check(out, ref, what=""):
+    out = out.float().cpu().numpy()
+    diff = np.abs(out - ref)
+    mx = float(diff.max()) if diff.size else 0.0
+    rel = float(np.linalg.norm(out - ref) / max(np.linalg.norm(ref), 1e-30))
+    assert np.isfinite(out).all(), f"{what}: non-finite output"
+    assert mx <= MAX_ABS and rel <= REL_L2, f"{what}: max_abs={mx:.3e} rel_l2={rel:.3e} at {np.unravel_index(diff.argmax(), diff.shape)}"
+    return mx, rel
+
+
+def run_case(H, S, d, pattern, dmin, dmax, seed, Sk=None, lse=True):
+    Sk = Sk or S
+    nq, nk = -(-S // 64), -(-Sk // 64)
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, pattern, dmin, dmax, 1.0, seed))
+    q, k, v = make_qkv(S, H, d, seed, Sk)
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                           masks.words, nk)
+    out, out_lse = sparse_attention(q.cuda(), k.cuda(), v.cuda(), masks, return_lse=True)
+    torch.cuda.synchronize()
+    mx, rel = check(out, ref, f"H{H} S{S} Sk{Sk} d{d} {pattern}")
+    if lse:
+        ol = out_lse.cpu().numpy()
+        fin = np.isfinite(ref_lse)
+        assert np.array_equal(fin, np.isfinite(ol)), "LSE -inf pattern differs"
+        assert np.abs(ol[fin] - ref_lse[fin]).max() < 1e-2
+    return mx, rel
+
+
+def test_config_a_toy():
+    # BASELINE config A: 8 heads, 4096 tokens, d=64, 50% random block mask.
+    run_case(8, 4096, 64, "random", 0.5, 0.5, 1)
+
+
+@pytest.mark.parametrize("pattern", ["random", "banded", "clustered"])
+def test_d128_patterns(pattern):
+    run_case(4, 2048, 128, pattern, 0.1, 0.6, 3)
+
+
+def test_ragged_tokens_and_single_tail_block():
+    run_case(3, 1000, 64, "random", 0.3, 0.7, 5)            # odd number of Q blocks, partial tail
+    run_case(2, 4100, 128, "clustered", 0.2, 0.5, 6, Sk=3000)  # Sq != Sk, both ragged
+
+
+def test_dense_and_empty_rows():
+    H, S, d = 2, 1024, 128
+    nq = nk = S // 64
+    dense = np.ones((H, nq, nk), bool)
+    dense[0, 3, :] = False          # a Q block with no dense tile -> O = 0, LSE = -inf
+    dense[1, :, 5] = False
+    masks = D.AttentionMaskSet.from_dense(dense)
+    q, k, v = make_qkv(S, H, d, 9)
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                           masks.words, nk)
+    out, lse = sparse_attention(q.cuda(), k.cuda(), v.cuda(), masks, return_lse=True)
+    torch.cuda.synchronize()
+    check(out, ref, "dense/empty")
+    assert torch.all(out[3 * 64:4 * 64, 0] == 0)
+    assert torch.all(torch.isinf(lse[0, 3 * 64:4 * 64]))
+
+
+def test_large_scores_rescale_path():
+    # Growing score scale forces the lazy O rescale (max grows by > 2^8).
+    H, S, d = 2, 2048, 64
+    nq = nk = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, "random", 0.6, 0.6, 1.0, 4))
+    q, k, v = make_qkv(S, H, d, 10)
+    ramp = torch.linspace(0.2, 6.0, S).view(S, 1, 1)
+    k = (k.float() * ramp).to(torch.bfloat16)
+    ref, _ = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                     masks.words, nk)
+    out = sparse_attention(q.cuda(), k.cuda(), v.cuda(), masks)
+    torch.cuda.synchronize()
+    check(out, ref, "rescale")
+
+
+def test_ring_accumulate_equals_full():
+    # Two "ring periods" over disjoint KV-block groups merged in the epilogue
+    # reproduce the one-shot result (ring merge).
+    H, S, d = 4, 2048, 128
+    nq = nk = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, "clustered", 0.2, 0.6, 1.0, 12))
+    q, k, v = make_qkv(S, H, d, 13)
+    ref, _ = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                     masks.words, nk)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    o_acc = torch.empty(S, H, d, dtype=torch.float32, device="cuda")
+    l_acc = torch.empty(H, S, dtype=torch.float32, device="cuda")
+    out = torch.empty_like(qd)
+    accum_init(o_acc, l_acc)
+    groups = [np.arange(0, nk, 2), np.arange(1, nk, 2)]
+    scheds = []
+    for i, g in enumerate(groups):
+        kv_local = torch.cat([kd[b * 64:(b + 1) * 64] for b in g]).contiguous()
+        vv_local = torch.cat([vd[b * 64:(b + 1) * 64] for b in g]).contiguous()
+        sc = AttentionSchedule().build(masks, kv_block_ids=g, kv_tokens_global=S)
+        sc.launch(qd, kv_local, vv_local, out, o_accum=o_acc, lse_accum=l_acc, accumulate=True,
+                  finalize=(i == len(groups) - 1))
+        scheds.append((sc, kv_local, vv_local))
+    torch.cuda.synchronize()
+    check(out, ref, "ring-accumulate")
+
+
+def test_mask_stats_device_exact():
+    m = D.generate_mask_set(D.GeneratorSpec(40, 512, 512, 64, "clustered", 0.15, 0.45, 1.0, 1))
+    words = torch.from_numpy(m.words.view(np.int64)).cuda()
+    hc, rw, cw = D.mask_stats_device(words, 512)
+    grid = D.summed_grid(m).reshape(512, 512).astype(np.int64)
+    assert hc.cpu().tolist() == D.blocks_per_head(m)
+    assert rw.cpu().numpy().tolist() == grid.sum(1).tolist()
+    assert cw.cpu().numpy().tolist() == grid.sum(0).tolist()
+
+
+def test_errors_are_loud():
+    m = D.generate_mask_set(D.GeneratorSpec(2, 4, 4, 64, "random", 0.5, 0.5, 1.0, 1))
+    q, k, v = make_qkv(256, 2, 96, 1)
+    with pytest.raises(D.ConfigError):
+        sparse_attention(q.cuda(), k.cuda(), v.cuda(), m)
+    q, k, v = make_qkv(256, 2, 64, 1)
+    with pytest.raises(D.ContractError):
+        sparse_attention(q, k, v, m)  # CPU tensors: no fallback
