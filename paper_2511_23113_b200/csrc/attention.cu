@@ -63,7 +63,7 @@ struct KCfg {
   static constexpr uint32_t kQChunk = 128u * 128u;    // one 64-column chunk of Q
   static constexpr uint32_t kTileBytes = 64u * D * 2u;
   static constexpr int kStages = D == 128 ? 2 : 4;
-  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 2 + 1;
+  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 2 + 2;
   static constexpr uint32_t kDataBytes = kQBytes + 2u * kStages * kTileBytes;
   static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
 };
@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   auto bVempty = [&](int s) { return sBar + 8u * (1 + 3 * NS + s); };
   auto bSfull = [&](int b) { return sBar + 8u * (1 + 4 * NS + b); };
   auto bPfull = [&](int b) { return sBar + 8u * (3 + 4 * NS + b); };
-  const uint32_t bOdone = sBar + 8u * (5 + 4 * NS);
+  const uint32_t bOdone = sBar + 8u * (5 + 4 * NS);   // one phase per PV_j
+  const uint32_t bOfinal = sBar + 8u * (6 + 4 * NS);  // single phase: every PV done
   const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
 
   const int warp = threadIdx.x >> 5;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(bPfull(b), 128);
     }
     mbar_init(bOdone, 1);
+    mbar_init(bOfinal, 1);
     mbar_fence_init();
   }
   if (warp == 4 && lane == 0) {
@@ -182,6 +184,12 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_after();
       for (uint32_t j = 0; j < count; ++j) {
         const int s = int(j % NS);
+        // S_j overwrites the TMEM columns that hold P_{j-2}; PV_{j-2} (issued
+        // just before) must have finished reading them (WAR across MMAs is not
+        // ordered by issue order).  Completed PVs here are j-2 or j-1.
+#ifndef DBSP_NO_WAR_WAIT
+        if (j >= 2) mbar_wait(bOdone, (j - 2) & 1);
+#endif
         mbar_wait(bKfull(s), (j / NS) & 1);
         tc_fence_after();
         const uint32_t dcol = tmem + ((j & 1) ? kColS1 : kColS0);
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (j > 0) pv(j - 1);
       }
       pv(count - 1);
+      tc_commit(bOfinal);
     }
     __syncwarp();
   } else {
@@ -274,7 +283,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     // ------------------------------------------------------------ epilogue
     if (count > 0) {
-      mbar_wait(bOdone, (count - 1) & 1);
+      // Not bOdone: up to two PV phases may still be outstanding here, and a
+      // parity wait cannot tell phase count-1 from phase count-3.
+      mbar_wait(bOfinal, 0);
       tc_fence_after();
     }
     const uint32_t qblk = upper ? it.qb : it.qa;
