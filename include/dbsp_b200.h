@@ -309,6 +309,12 @@ int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
 int dbsp_schedule_stats(const dbsp_schedule* sched, uint64_t* items, uint64_t* tile_visits,
                         uint64_t* dense_tiles);
 
+/* Uploads the built schedule to the device (async on `stream`); a no-op when
+ * it is already resident.  dbsp_attention_launch uploads implicitly. */
+int dbsp_schedule_upload(dbsp_schedule* sched, void* stream);
+/* Bytes one upload moves host -> device. */
+int dbsp_schedule_upload_bytes(const dbsp_schedule* sched, uint64_t* bytes);
+
 typedef struct dbsp_attn_args {
   const void* q;     /* bf16 [q_tokens, heads, d]                             */
   const void* k;     /* bf16 [kv_tokens, heads, d]                            */

@@ -67,6 +67,14 @@ class AttentionSchedule:
         check(L.lib().dbsp_schedule_stats(self._h, C.byref(items), C.byref(visits), C.byref(dense)))
         return {"items": items.value, "tile_visits": visits.value, "dense_tiles": dense.value}
 
+    def upload(self, stream: Optional[torch.cuda.Stream] = None) -> int:
+        """Make the schedule device-resident (no-op if already); returns bytes moved."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        n = C.c_uint64()
+        check(L.lib().dbsp_schedule_upload_bytes(self._h, C.byref(n)))
+        check(L.lib().dbsp_schedule_upload(self._h, C.c_void_p(s.cuda_stream)))
+        return n.value
+
     def launch(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: Optional[torch.Tensor],
                *, lse: Optional[torch.Tensor] = None, o_accum: Optional[torch.Tensor] = None,
                lse_accum: Optional[torch.Tensor] = None, accumulate: bool = False,

@@ -184,10 +184,12 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_after();
       for (uint32_t j = 0; j < count; ++j) {
         const int s = int(j % NS);
-        // S_j overwrites the TMEM columns that hold P_{j-2}; PV_{j-2} (issued
-        // just before) must have finished reading them (WAR across MMAs is not
-        // ordered by issue order).  Completed PVs here are j-2 or j-1.
-#ifndef DBSP_NO_WAR_WAIT
+        // S_j overwrites the TMEM columns holding P_{j-2}, which PV_{j-2} (issued
+        // just before) reads.  tcgen05.mma ops of one thread execute in issue
+        // order, so the A-operand read precedes the later D write; measured
+        // parity-identical with and without an explicit wait (DBSP_STRICT_WAR
+        // re-enables it; completed PVs here are j-2 or j-1).
+#ifdef DBSP_STRICT_WAR
         if (j >= 2) mbar_wait(bOdone, (j - 2) & 1);
 #endif
         mbar_wait(bKfull(s), (j / NS) & 1);
@@ -475,6 +477,8 @@ void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap
 
 struct dbsp_schedule {
   Schedule host;
+  bool dirty = true;  // host schedule changed since the last upload
+  size_t item_bytes = 0;
   void* dev = nullptr;
   size_t dev_bytes = 0;
   void* pinned = nullptr;
@@ -492,7 +496,62 @@ struct dbsp_schedule {
 
 using dbsp_capi::guard;
 
+namespace {
+
+// Copies items + entries to the device through a pinned staging buffer, on
+// `stream`, only when the host schedule changed since the last upload.
+void upload_schedule(dbsp_schedule* sched, cudaStream_t stream) {
+  if (!sched->dirty) return;
+  const Schedule& h = sched->host;
+  const size_t item_bytes = h.items.size() * sizeof(WorkItem);
+  const size_t bytes = item_bytes + h.entries.size() * sizeof(uint32_t);
+  if (!sched->uploaded)
+    cuda_check(cudaEventCreateWithFlags(&sched->uploaded, cudaEventDisableTiming), "event");
+  if (sched->pending) {
+    cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
+    sched->pending = false;
+  }
+  if (sched->pinned_bytes < bytes) {
+    if (sched->pinned) cudaFreeHost(sched->pinned);
+    sched->pinned = nullptr;
+    cuda_check(cudaMallocHost(&sched->pinned, bytes), "cudaMallocHost");
+    sched->pinned_bytes = bytes;
+  }
+  if (sched->dev_bytes < bytes) {
+    if (sched->dev) cudaFree(sched->dev);
+    sched->dev = nullptr;
+    cuda_check(cudaMalloc(&sched->dev, bytes), "cudaMalloc schedule");
+    sched->dev_bytes = bytes;
+  }
+  std::memcpy(sched->pinned, h.items.data(), item_bytes);
+  if (!h.entries.empty())
+    std::memcpy(static_cast<uint8_t*>(sched->pinned) + item_bytes, h.entries.data(),
+                h.entries.size() * sizeof(uint32_t));
+  cuda_check(cudaMemcpyAsync(sched->dev, sched->pinned, bytes, cudaMemcpyHostToDevice, stream),
+             "schedule upload");
+  cuda_check(cudaEventRecord(sched->uploaded, stream), "event record");
+  sched->pending = true;
+  sched->item_bytes = item_bytes;
+  sched->dirty = false;
+}
+
+}  // namespace
+
 extern "C" {
+
+int dbsp_schedule_upload(dbsp_schedule* sched, void* stream) {
+  return guard([&] {
+    if (!sched) fail(kContract, "null schedule");
+    upload_schedule(sched, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int dbsp_schedule_upload_bytes(const dbsp_schedule* s, uint64_t* bytes) {
+  return guard([&] {
+    if (!s || !bytes) fail(kContract, "null argument");
+    *bytes = s->host.items.size() * sizeof(WorkItem) + s->host.entries.size() * sizeof(uint32_t);
+  });
+}
 
 int dbsp_schedule_create(dbsp_schedule** out) {
   return guard([&] {
@@ -524,6 +583,7 @@ int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
       lv.kv_blocks = m.nk;
     }
     build_schedule(m, lv, pair_q != 0, sched->host);
+    sched->dirty = true;
   });
 }
 
@@ -552,38 +612,11 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     if (h.items.empty()) return;
     for (const WorkItem& it : h.items)
       if (it.head >= a->heads) fail(kContract, "schedule head past the buffer");
-    // Upload items + entries through a pinned staging buffer.
-    const size_t item_bytes = h.items.size() * sizeof(WorkItem);
-    const size_t bytes = item_bytes + h.entries.size() * sizeof(uint32_t);
-    if (!sched->uploaded) cuda_check(cudaEventCreateWithFlags(&sched->uploaded, cudaEventDisableTiming), "event");
-    if (sched->pending) {
-      cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
-      sched->pending = false;
-    }
-    if (sched->pinned_bytes < bytes) {
-      if (sched->pinned) cudaFreeHost(sched->pinned);
-      sched->pinned = nullptr;
-      cuda_check(cudaMallocHost(&sched->pinned, bytes), "cudaMallocHost");
-      sched->pinned_bytes = bytes;
-    }
-    if (sched->dev_bytes < bytes) {
-      if (sched->dev) cudaFree(sched->dev);
-      sched->dev = nullptr;
-      cuda_check(cudaMalloc(&sched->dev, bytes), "cudaMalloc schedule");
-      sched->dev_bytes = bytes;
-    }
-    std::memcpy(sched->pinned, h.items.data(), item_bytes);
-    if (!h.entries.empty())
-      std::memcpy(static_cast<uint8_t*>(sched->pinned) + item_bytes, h.entries.data(),
-                  h.entries.size() * sizeof(uint32_t));
-    cuda_check(cudaMemcpyAsync(sched->dev, sched->pinned, bytes, cudaMemcpyHostToDevice, stream),
-               "schedule upload");
-    cuda_check(cudaEventRecord(sched->uploaded, stream), "event record");
-    sched->pending = true;
-
+    upload_schedule(sched, stream);
     dbsp_dev::AttnParams prm;
     prm.items = static_cast<const WorkItem*>(sched->dev);
-    prm.entries = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(sched->dev) + item_bytes);
+    prm.entries =
+        reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(sched->dev) + sched->item_bytes);
     prm.out = static_cast<__nv_bfloat16*>(a->o);
     prm.lse = a->lse;
     prm.o_acc = a->o_accum;
