@@ -65,7 +65,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if force or _stale(obj, [CSRC / src] + headers):
             extra = os.environ.get("DBSP_NVCC_FLAGS", "").split()
             cmd = [nvcc, GENCODE, "-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
-                   "-DDBSP_WATCHDOG", *extra,
+                   *extra,
                    "-Xcompiler", "-ffp-contract=off", f"-I{ROOT / 'include'}", "-c", str(CSRC / src),
                    "-o", str(obj)]
             if verbose:

@@ -55,6 +55,10 @@ constexpr uint32_t kColO = 0;
 constexpr uint32_t kColS0 = 128;
 constexpr uint32_t kColS1 = 192;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain
+#ifndef DBSP_POLY_EVERY
+#define DBSP_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = DBSP_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
 
 template <int D>
 struct KCfg {
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bSfull(b), 1);
-      mbar_init(bPfull(b), 128);
+      mbar_init(bPfull(b), 4);  // one arrive per softmax warp
     }
     mbar_init(bOdone, 1);
     mbar_init(bOfinal, 1);
@@ -233,12 +237,27 @@ __global__ void __launch_bounds__(kThreads, 2)
         tmem_ld_wait();
         const uint32_t valid = ((e >> dbsp_core::kEntryValidShift) & 63u) + 1u;
         float v[64];
-        float mt = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          v[i] = (uint32_t(i) < valid) ? __uint_as_float(i < 32 ? sa[i] : sb[i - 32]) : -INFINITY;
-          mt = fmaxf(mt, v[i]);
+        for (int i = 0; i < 32; ++i) {
+          v[i] = __uint_as_float(sa[i]);
+          v[i + 32] = __uint_as_float(sb[i]);
         }
+        if (valid < 64) {  // partial last KV block (warp-uniform)
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (uint32_t(i) >= valid) v[i] = -INFINITY;
+        }
+        // Row max as a 3-input-max tree (FMNMX3): depth 5 instead of a 64-long chain.
+        float mx[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          mx[a] = fmax3f(v[8 * a], v[8 * a + 1], v[8 * a + 2]);
+          mx[a] = fmax3f(mx[a], v[8 * a + 3], v[8 * a + 4]);
+          mx[a] = fmax3f(mx[a], v[8 * a + 5], v[8 * a + 6]);
+          mx[a] = fmaxf(mx[a], v[8 * a + 7]);
+        }
+        const float mt = fmaxf(fmax3f(mx[0], mx[1], mx[2]),
+                               fmax3f(fmax3f(mx[3], mx[4], mx[5]), mx[6], mx[7]));
         const float mt2 = mt * sl2;
         const bool resc = mt2 > m + kRescaleThreshold;
         const bool need_o = resc && (m != -INFINITY);
@@ -263,16 +282,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             tmem_st32(tmem + lane_off + kColO + c * 32, o);
           }
         }
+        // exp2 split between the MUFU (ex2.approx) and a degree-3 polynomial
+        // on the FMA pipe for every kPolyEvery-th pair (FA4-style offload:
+        // MUFU is 16/clk/SM, the FMA pipe is otherwise idle here).
         const float negm = -m;
-        float sum = 0.f;
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float p0 = fast_exp2(fmaf(v[2 * i], sl2, negm));
-          const float p1 = fast_exp2(fmaf(v[2 * i + 1], sl2, negm));
-          sum += p0 + p1;
+          const float x0 = fmaf(v[2 * i], sl2, negm);
+          const float x1 = fmaf(v[2 * i + 1], sl2, negm);
+          float p0, p1;
+          if ((i % kPolyEvery) == kPolyEvery - 1) {
+            p0 = exp2_poly3(x0);
+            p1 = exp2_poly3(x1);
+          } else {
+            p0 = fast_exp2(x0);
+            p1 = fast_exp2(x1);
+          }
+          sum4[i & 3] += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
         }
-        l += sum;
+        l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) pk[i] = 0u;
@@ -280,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       tmem_st32(scol, pk);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(bPfull(int(j & 1)));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bPfull(int(j & 1)));
     }
 
     // ------------------------------------------------------------ epilogue

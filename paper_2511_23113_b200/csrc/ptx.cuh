@@ -188,6 +188,26 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x on the FMA/ALU pipes: x = n + f, f in [-0.5, 0.5]; 2^f by a degree-3
+// minimax polynomial (max rel. error 1.0e-4, far below bf16's 2^-9), 2^n by
+// adding n to the exponent field.  x <= -127 flushes to 0 like ex2.approx.ftz.
+__device__ __forceinline__ float exp2_poly3(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: integer part lands in the low bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.05500764772295952f, 0.24220800399780273f);
+  p = fmaf(p, f, 0.6932827234268188f);
+  p = fmaf(p, f, 1.0f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
