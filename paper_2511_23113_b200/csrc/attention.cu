@@ -47,7 +47,24 @@ struct AttnParams {
   uint32_t heads;
   uint32_t mode;
   float scale_log2;
+  unsigned long long* trace;  // DBSP_TRACE builds only: clock64 per (block, tile, event)
 };
+
+// Event slots of the optional per-tile trace (DBSP_TRACE).
+enum : int { kTrSoftStart = 0, kTrSoftEnd, kTrMmaS, kTrMmaPV, kTrSoftStartHi, kTrSoftEndHi,
+             kTrLoadK, kTrLoadV, kTrEvents };
+constexpr int kTraceBlocks = 16, kTraceTiles = 256;
+#ifdef DBSP_TRACE
+#define DBSP_TR(ev, j)                                                                         \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x < kTraceBlocks && (j) < kTraceTiles)                             \
+      p.trace[(size_t(blockIdx.x) * kTraceTiles + (j)) * kTrEvents + (ev)] = clock64();        \
+  } while (0)
+#else
+#define DBSP_TR(ev, j) \
+  do {                 \
+  } while (0)
+#endif
 
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
@@ -154,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = int(j % NS);
         mbar_wait(bKempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmK, sK + s * C::kTileBytes, bKfull(s), j);
+        DBSP_TR(kTrLoadK, j);
       };
       load_k(0);
       for (uint32_t j = 0; j < count; ++j) {
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = int(j % NS);
         mbar_wait(bVempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmV, sV + s * C::kTileBytes, bVfull(s), j);
+        DBSP_TR(kTrLoadV, j);
       }
     }
     __syncwarp();
@@ -183,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         tc_commit(bVempty(s));
         tc_commit(bOdone);
+        DBSP_TR(kTrMmaPV, i);
       };
       mbar_wait(bQ, 0);
       tc_fence_after();
@@ -208,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         tc_commit(bKempty(s));
         tc_commit(bSfull(int(j & 1)));
+        DBSP_TR(kTrMmaS, j);
         if (j > 0) pv(j - 1);
       }
       pv(count - 1);
@@ -228,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const bool dense = (e & dense_bit) != 0;  // warp-uniform (one half per warp)
       const uint32_t scol = tmem + lane_off + ((j & 1) ? kColS1 : kColS0);
       mbar_wait(bSfull(int(j & 1)), (j >> 1) & 1);
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftStart : kTrSoftStartHi, j);
       tc_fence_after();
       uint32_t pk[32];
       if (dense) {
@@ -312,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bPfull(int(j & 1)));
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftEnd : kTrSoftEndHi, j);
     }
 
     // ------------------------------------------------------------ epilogue
@@ -529,6 +552,8 @@ using dbsp_capi::guard;
 
 namespace {
 
+unsigned long long* g_trace = nullptr;
+
 // Copies items + entries to the device through a pinned staging buffer, on
 // `stream`, only when the host schedule changed since the last upload.
 void upload_schedule(dbsp_schedule* sched, cudaStream_t stream) {
@@ -657,6 +682,7 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     prm.mode = (acc ? dbsp_dev::kModeAccumulate : 0u) | (a->finalize ? dbsp_dev::kModeFinalize : 0u);
     const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(float(a->head_dim));
     prm.scale_log2 = scale * 1.4426950408889634f;
+    prm.trace = g_trace;
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
@@ -684,6 +710,13 @@ int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, 
   const int rc = dbsp_schedule_build(sched, set, &v, 1);
   if (rc) return rc;
   return dbsp_attention_launch(sched, args, stream);
+}
+
+// Debug hook (not in the public header): device buffer of
+// 16 blocks x 256 tiles x 8 events u64 clock64 stamps, used by DBSP_TRACE builds.
+int dbsp_debug_set_trace(unsigned long long* dev) {
+  g_trace = dev;
+  return 0;
 }
 
 int dbsp_accum_init(float* o_accum, float* lse_accum, uint32_t q_tokens, uint32_t heads,
