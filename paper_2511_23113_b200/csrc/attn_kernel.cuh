@@ -1,0 +1,455 @@
+// K4: block-sparse FlashAttention forward for sm_100a (tcgen05 + TMEM + TMA).
+//
+// One CTA = one work item (schedule.hpp): a 128-row Q tile (two 64-row Q
+// blocks of one head) against the union of their dense 64-key KV blocks.
+// Two CTAs per SM, so one CTA's softmax overlaps the other's MMAs.
+// Warp roles (192 threads):
+//   warps 0-3  Q -> TMEM at start; softmax; epilogue.  Thread t owns Q row t
+//              (TMEM lane t).
+//   warp 4     TMA producer: K and V tiles through an NS-deep smem ring.
+//   warp 5     TMEM allocator + single-thread tcgen05.mma issuer.
+// Per KV tile j:
+//   S_j = Q K_j^T        tcgen05.mma TS: A = Q from TMEM, B = K (smem, SW128),
+//                        M=128 N=64 K=d -> TMEM S[j % NSB]
+//   P_j = exp2(S_j*c-m)  softmax warps; bf16 P written over S[j % NSB]
+//   O  += P_j V_j        tcgen05.mma TS: A = P from TMEM, B = V (smem, MN-major)
+// Q lives in TMEM rather than shared memory: an SS-mode QK^T with N=64 reads
+// 6 KB of smem per 32-cycle MMA (192 B/clk, above the 128 B/clk smem port),
+// which capped the first version at ~55% tensor activity.  With A in TMEM the
+// per-tile smem traffic is K + V reads + their TMA writes = 64 KB / 512 MMA
+// cycles.  The online-softmax max is rescaled lazily (only when it grows by
+// more than 2^8), so O in TMEM is touched by the softmax warps only rarely.
+// Mask semantics follow the reference BlockMask (mask.hpp:18-20): a tile is
+// computed iff its bit is set; everything else contributes exactly zero.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "schedule.hpp"
+
+namespace dbsp_dev {
+
+using dbsp_core::WorkItem;
+
+enum : uint32_t { kModeAccumulate = 1, kModeFinalize = 2 };
+
+struct AttnParams {
+  const WorkItem* items;
+  const uint32_t* entries;
+  const __nv_bfloat16* q;  // [q_tokens, heads, D]
+  __nv_bfloat16* out;
+  float* lse;
+  float* o_acc;
+  float* lse_acc;
+  uint32_t q_tokens;
+  uint32_t heads;
+  uint32_t mode;
+  float scale_log2;
+  unsigned long long* trace;  // DBSP_TRACE builds only: clock64 per (block, tile, event)
+};
+
+// Event slots of the optional per-tile trace (DBSP_TRACE).
+enum : int { kTrSoftStart = 0, kTrSoftEnd, kTrMmaS, kTrMmaPV, kTrSoftStartHi, kTrSoftEndHi,
+             kTrLoadK, kTrLoadV, kTrEvents };
+constexpr int kTraceBlocks = 16, kTraceTiles = 256;
+#ifdef DBSP_TRACE
+#define DBSP_TR(ev, j)                                                                         \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x < kTraceBlocks && (j) < kTraceTiles)                             \
+      p.trace[(size_t(blockIdx.x) * kTraceTiles + (j)) * kTrEvents + (ev)] = clock64();        \
+  } while (0)
+#else
+#define DBSP_TR(ev, j) \
+  do {                 \
+  } while (0)
+#endif
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTmemCols = 256;
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain
+#ifndef DBSP_POLY_EVERY
+#define DBSP_POLY_EVERY 1000
+#endif
+constexpr int kPolyEvery = DBSP_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
+
+template <int D>
+struct KCfg {
+  static constexpr int kChunks = D / 64;  // 128-byte swizzle atoms along d
+  static constexpr uint32_t kTileBytes = 64u * D * 2u;
+  // TMEM columns (256 per CTA): Q (bf16, D/2 cols), NSB S/P buffers of 64
+  // cols, O (fp32, D cols); regions 64-column aligned.
+  static constexpr int kNSB = D == 128 ? 1 : 2;
+  static constexpr uint32_t kColQ = 0;
+  static constexpr uint32_t kColS = 64;
+  static constexpr uint32_t kColO = 64 + 64 * kNSB;
+  static_assert(kColO + D <= kTmemCols, "TMEM budget");
+  static constexpr int kStages = D == 128 ? 3 : 6;  // K/V smem ring depth
+  static constexpr int kNumBars = 4 * kStages + 2 * kNSB + 3;
+  static constexpr uint32_t kDataBytes = 2u * kStages * kTileBytes;
+  static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2)
+    sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = KCfg<D>;
+  constexpr int NS = C::kStages;
+  constexpr int NSB = C::kNSB;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+
+  const uint32_t sK = base;
+  const uint32_t sV = sK + NS * C::kTileBytes;
+  const uint32_t sBar = sV + NS * C::kTileBytes;
+  auto bKfull = [&](int s) { return sBar + 8u * s; };
+  auto bVfull = [&](int s) { return sBar + 8u * (NS + s); };
+  auto bKempty = [&](int s) { return sBar + 8u * (2 * NS + s); };
+  auto bVempty = [&](int s) { return sBar + 8u * (3 * NS + s); };
+  auto bSfull = [&](int b) { return sBar + 8u * (4 * NS + b); };
+  auto bPfull = [&](int b) { return sBar + 8u * (4 * NS + NSB + b); };
+  const uint32_t bQready = sBar + 8u * (4 * NS + 2 * NSB);      // Q written to TMEM
+  const uint32_t bOdone = sBar + 8u * (4 * NS + 2 * NSB + 1);   // one phase per PV_j
+  const uint32_t bOfinal = sBar + 8u * (4 * NS + 2 * NSB + 2);  // single phase: all PVs done
+  const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const WorkItem it = p.items[blockIdx.x];
+  const uint32_t count = it.count;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(bKfull(s), 1);
+      mbar_init(bVfull(s), 1);
+      mbar_init(bKempty(s), 1);
+      mbar_init(bVempty(s), 1);
+    }
+    for (int b = 0; b < NSB; ++b) {
+      mbar_init(bSfull(b), 1);
+      mbar_init(bPfull(b), 4);  // one arrive per softmax warp
+    }
+    mbar_init(bQready, 4);
+    mbar_init(bOdone, 1);
+    mbar_init(bOfinal, 1);
+    mbar_fence_init();
+  }
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
+  if (warp == 5) tmem_alloc(sTmemSlot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(gbase + (sTmemSlot - base));
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0 && count > 0) {
+      const uint64_t pol_kv = l2_policy_evict_last();
+      const int head = int(it.head);
+      const uint32_t* ent = p.entries + it.begin;
+      auto load_tile = [&](const CUtensorMap* tm, uint32_t dst, uint32_t full, uint32_t j) {
+        const int kv = int(__ldg(ent + j) & dbsp_core::kEntryKvMask);
+        mbar_expect_tx(full, C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(dst + c * 8192, tm, c * 64, head, kv * 64, full, pol_kv);
+      };
+      auto load_k = [&](uint32_t j) {
+        const int s = int(j % NS);
+        mbar_wait(bKempty(s), ((j / NS) & 1) ^ 1);
+        load_tile(&tmK, sK + s * C::kTileBytes, bKfull(s), j);
+        DBSP_TR(kTrLoadK, j);
+      };
+      load_k(0);
+      for (uint32_t j = 0; j < count; ++j) {
+        if (j + 1 < count) load_k(j + 1);  // K runs one tile ahead of V
+        const int s = int(j % NS);
+        mbar_wait(bVempty(s), ((j / NS) & 1) ^ 1);
+        load_tile(&tmV, sV + s * C::kTileBytes, bVfull(s), j);
+        DBSP_TR(kTrLoadV, j);
+      }
+    } else if (count > 0) {
+      mbar_wait(bOfinal, 0);  // idle lanes sleep on an mbarrier, not in a warp-sync spin
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && count > 0) {
+      constexpr uint32_t kIdescQK = idesc_bf16(128, 64, false, false);
+      constexpr uint32_t kIdescPV = idesc_bf16(128, D, false, true);
+      auto issue_s = [&](uint32_t j) {
+        const int s = int(j % NS);
+        mbar_wait(bKfull(s), (j / NS) & 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + C::kColS + 64u * (j % NSB);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t bd =
+              smem_desc_sw128(sK + s * C::kTileBytes + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
+          mma_ts(dcol, tmem + C::kColQ + kk * 8, bd, kIdescQK, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(bKempty(s));
+        tc_commit(bSfull(int(j % NSB)));
+        DBSP_TR(kTrMmaS, j);
+      };
+      auto issue_pv = [&](uint32_t i) {
+        const int b = int(i % NSB);
+        const int s = int(i % NS);
+        mbar_wait(bPfull(b), (i / NSB) & 1);
+        mbar_wait(bVfull(s), (i / NS) & 1);
+        tc_fence_after();
+        const uint32_t pcol = tmem + C::kColS + 64u * b;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t bd = smem_desc_sw128(sV + s * C::kTileBytes + kk * 2048, 8192, 1024);
+          mma_ts(tmem + C::kColO, pcol + kk * 8, bd, kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(bVempty(s));
+        tc_commit(bOdone);
+        DBSP_TR(kTrMmaPV, i);
+      };
+      mbar_wait(bQready, 0);
+      tc_fence_after();
+      // S runs NSB tiles ahead of PV.  S_{j+NSB} reuses the TMEM columns of
+      // P_j, which PV_j (issued just before) reads: tcgen05.mma ops of one
+      // thread execute in issue order, so that read precedes the later write
+      // (DBSP_STRICT_WAR adds an explicit completion wait).
+      for (uint32_t j = 0; j < uint32_t(NSB) && j < count; ++j) issue_s(j);
+      for (uint32_t j = 0; j < count; ++j) {
+        issue_pv(j);
+        if (j + NSB < count) {
+#ifdef DBSP_STRICT_WAR
+          mbar_wait(bOdone, j & 1);
+#endif
+          issue_s(j + NSB);
+        }
+      }
+      tc_commit(bOfinal);
+    } else if (count > 0) {
+      mbar_wait(bOfinal, 0);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ Q -> TMEM
+    const int row = threadIdx.x;  // 0..127 == TMEM lane
+    const bool upper = row >= 64;
+    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+    const uint32_t qblk = upper ? it.qb : it.qa;
+    const uint32_t token = qblk * 64u + uint32_t(row & 63);
+    if (count > 0) {
+      const bool in = token < p.q_tokens;
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (size_t(token) * p.heads + it.head) * D);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 x = in ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
+          w[4 * i + 0] = x.x;
+          w[4 * i + 1] = x.y;
+          w[4 * i + 2] = x.z;
+          w[4 * i + 3] = x.w;
+        }
+        tmem_st32(tmem + lane_off + C::kColQ + c * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bQready);
+    }
+
+    // ------------------------------------------------------------ softmax
+    const uint32_t dense_bit = upper ? dbsp_core::kEntryDenseB : dbsp_core::kEntryDenseA;
+    const float sl2 = p.scale_log2;
+    const uint32_t* ent = p.entries + it.begin;
+    float m = -INFINITY, l = 0.f;
+    for (uint32_t j = 0; j < count; ++j) {
+      const uint32_t e = __ldg(ent + j);
+      const bool dense = (e & dense_bit) != 0;  // warp-uniform (one half per warp)
+      const int b = int(j % NSB);
+      const uint32_t scol = tmem + lane_off + C::kColS + 64u * b;
+      mbar_wait(bSfull(b), (j / NSB) & 1);
+      tc_fence_after();
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftStart : kTrSoftStartHi, j);
+      uint32_t pk[32];
+      if (dense) {
+        uint32_t sa[32], sb[32];
+        tmem_ld32(scol, sa);
+        tmem_ld32(scol + 32, sb);
+        tmem_ld_wait();
+        const uint32_t valid = ((e >> dbsp_core::kEntryValidShift) & 63u) + 1u;
+        float v[64];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] = __uint_as_float(sa[i]);
+          v[i + 32] = __uint_as_float(sb[i]);
+        }
+        if (valid < 64) {  // partial last KV block (warp-uniform)
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (uint32_t(i) >= valid) v[i] = -INFINITY;
+        }
+        // Row max as a 3-input-max tree (FMNMX3): depth 5, not a 64-long chain.
+        float mx[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          mx[a] = fmax3f(v[8 * a], v[8 * a + 1], v[8 * a + 2]);
+          mx[a] = fmax3f(mx[a], v[8 * a + 3], v[8 * a + 4]);
+          mx[a] = fmax3f(mx[a], v[8 * a + 5], v[8 * a + 6]);
+          mx[a] = fmaxf(mx[a], v[8 * a + 7]);
+        }
+        const float mt = fmaxf(fmax3f(mx[0], mx[1], mx[2]),
+                               fmax3f(fmax3f(mx[3], mx[4], mx[5]), mx[6], mx[7]));
+        const float mt2 = mt * sl2;
+        const bool resc = mt2 > m + kRescaleThreshold;
+        const bool need_o = resc && (m != -INFINITY);
+        float alpha = 1.f;
+        if (resc) {
+          alpha = fast_exp2(m - mt2);
+          l *= alpha;
+          m = mt2;
+        }
+        if (__any_sync(0xffffffffu, need_o)) {
+          // O must be quiescent.  With one S buffer, S_j was issued after
+          // PV_{j-1}, so its completion (seen above) implies PV_{j-1}'s.
+          if (NSB > 1 && j > 0) {
+            mbar_wait(bOdone, (j - 1) & 1);  // completed PVs here: j-1 or j
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_off + C::kColO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tmem + lane_off + C::kColO + c * 32, o);
+          }
+        }
+        const float negm = -m;
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float x0 = fmaf(v[2 * i], sl2, negm);
+          const float x1 = fmaf(v[2 * i + 1], sl2, negm);
+          float p0, p1;
+          if ((i % kPolyEvery) == kPolyEvery - 1) {  // FA4-style MUFU offload (off by default)
+            p0 = exp2_poly3(x0);
+            p1 = exp2_poly3(x1);
+          } else {
+            p0 = fast_exp2(x0);
+            p1 = fast_exp2(x1);
+          }
+          sum4[i & 3] += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+      }
+      tmem_st32(scol, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bPfull(b));
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftEnd : kTrSoftEndHi, j);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    if (count > 0) {
+      // Not bOdone: up to two PV phases may still be outstanding here, and a
+      // parity wait cannot tell phase count-1 from phase count-3.
+      mbar_wait(bOfinal, 0);
+      tc_fence_after();
+    }
+    const bool live = !(upper && it.single) && token < p.q_tokens;
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    const float kLn2 = 0.6931471805599453f;
+    const float lse_new = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
+    const size_t orow = (size_t(token) * p.heads + it.head) * D;
+    const size_t lidx = size_t(it.head) * p.q_tokens + token;
+
+    float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
+    const bool acc = (p.mode & kModeAccumulate) != 0;
+    if (acc) {
+      const float lse_old = live ? p.lse_acc[lidx] : -INFINITY;
+      const float mx = fmaxf(lse_old, lse_new);
+      if (mx == -INFINITY) {
+        c_old = 0.f;
+        c_new = 0.f;
+        lse_out = -INFINITY;
+      } else {
+        const float w_old = __expf(lse_old - mx);
+        const float w_new = __expf(lse_new - mx);
+        const float den = w_old + w_new;
+        c_old = w_old / den;
+        c_new = w_new * inv_l / den;
+        lse_out = mx + __logf(den);
+      }
+    }
+    const bool write_bf16 = !acc || (p.mode & kModeFinalize);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      if (count > 0) {
+        tmem_ld32(tmem + lane_off + C::kColO + c * 32, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0u;
+      }
+      if (!live) continue;
+      float r[32];
+      if (acc) {
+        float4* pa = reinterpret_cast<float4*>(p.o_acc + orow + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4 a = pa[i];
+          a.x = a.x * c_old + __uint_as_float(o[4 * i + 0]) * c_new;
+          a.y = a.y * c_old + __uint_as_float(o[4 * i + 1]) * c_new;
+          a.z = a.z * c_old + __uint_as_float(o[4 * i + 2]) * c_new;
+          a.w = a.w * c_old + __uint_as_float(o[4 * i + 3]) * c_new;
+          pa[i] = a;
+          r[4 * i + 0] = a.x;
+          r[4 * i + 1] = a.y;
+          r[4 * i + 2] = a.z;
+          r[4 * i + 3] = a.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __uint_as_float(o[i]) * inv_l;
+      }
+      if (write_bf16) {
+        uint4* po = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          po[i] = make_uint4(pack_bf16x2(r[8 * i + 0], r[8 * i + 1]),
+                             pack_bf16x2(r[8 * i + 2], r[8 * i + 3]),
+                             pack_bf16x2(r[8 * i + 4], r[8 * i + 5]),
+                             pack_bf16x2(r[8 * i + 6], r[8 * i + 7]));
+      }
+    }
+    if (live) {
+      if (acc)
+        p.lse_acc[lidx] = lse_out;
+      else if (p.lse)
+        p.lse[lidx] = lse_new;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace dbsp_dev

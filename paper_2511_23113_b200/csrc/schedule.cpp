@@ -80,6 +80,9 @@ void build_schedule(const MaskView& m, const LocalView& v, bool pair_q, Schedule
   });
   out.items.clear();
   out.entries.clear();
+  out.max_head = v.heads - 1;
+  out.max_q_block = v.q_blocks - 1;
+  out.max_kv_block = v.kv_blocks - 1;
   out.items.reserve(raw.size());
   out.entries.reserve(out.tile_visits);
   for (uint32_t i : order) {

@@ -46,6 +46,7 @@ struct Schedule {
   std::vector<uint32_t> entries;
   uint64_t tile_visits = 0;  // sum of counts (MMA tiles issued)
   uint64_t dense_tiles = 0;  // 64x64 tiles actually dense (softmax work)
+  uint32_t max_head = 0, max_q_block = 0, max_kv_block = 0;  // bounds checked at launch
 };
 
 // Builds items ordered by local head, heaviest first within a head (keeps
