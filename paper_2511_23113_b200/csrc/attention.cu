@@ -101,7 +101,8 @@ CUtensorMap make_tmap(const void* ptr, uint32_t tokens, uint32_t heads, uint32_t
 }
 
 template <int D>
-void launch_kernel(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm,
+void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                   const dbsp_dev::AttnParams& prm,
                    uint32_t items, cudaStream_t stream) {
   using C = dbsp_dev::KCfg<D>;
   static std::once_flag once;
@@ -111,7 +112,7 @@ void launch_kernel(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::A
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute");
-  dbsp_dev::sparse_attn_fwd_kernel<D><<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
+  dbsp_dev::sparse_attn_fwd_kernel<D><<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd launch");
 }
 
@@ -277,12 +278,13 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(float(a->head_dim));
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.trace = g_trace;
+    const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
     if (a->head_dim == 128)
-      launch_kernel<128>(tk, tv, prm, uint32_t(h.items.size()), stream);
+      launch_kernel<128>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
     else
-      launch_kernel<64>(tk, tv, prm, uint32_t(h.items.size()), stream);
+      launch_kernel<64>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
   });
 }
 

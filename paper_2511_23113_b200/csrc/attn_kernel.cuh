@@ -79,22 +79,31 @@ template <int D>
 struct KCfg {
   static constexpr int kChunks = D / 64;  // 128-byte swizzle atoms along d
   static constexpr uint32_t kTileBytes = 64u * D * 2u;
-  // TMEM columns (256 per CTA): Q (bf16, D/2 cols), NSB S/P buffers of 64
-  // cols, O (fp32, D cols); regions 64-column aligned.
-  static constexpr int kNSB = D == 128 ? 1 : 2;
+  // Where Q lives.  d=64: in TMEM (TS-mode QK^T; 32 cols) -- measured 1.17x
+  // faster on the CogVideoX layer.  d=128: Q in TMEM (64 cols) would leave
+  // room for only one S buffer next to the 128-col O, which serialises
+  // softmax and MMA inside a CTA (measured 1.24x slower than Q in smem with
+  // two S buffers), so Q stays in smem (SS-mode QK^T) there.
+  static constexpr bool kQInTmem = D == 64;
+  static constexpr uint32_t kQBytes = kQInTmem ? 0u : 128u * D * 2u;
+  static constexpr uint32_t kQChunk = 128u * 128u;  // one 64-column chunk of a 128-row Q tile
+  // TMEM columns (256 per CTA): [Q], NSB S/P buffers of 64 cols, O (fp32, D
+  // cols); regions 64-column aligned.
+  static constexpr int kNSB = 2;
   static constexpr uint32_t kColQ = 0;
-  static constexpr uint32_t kColS = 64;
-  static constexpr uint32_t kColO = 64 + 64 * kNSB;
+  static constexpr uint32_t kColS = kQInTmem ? 64 : 0;
+  static constexpr uint32_t kColO = kColS + 64 * kNSB;
   static_assert(kColO + D <= kTmemCols, "TMEM budget");
-  static constexpr int kStages = D == 128 ? 3 : 6;  // K/V smem ring depth
+  static constexpr int kStages = D == 128 ? 2 : 6;  // K/V smem ring depth
   static constexpr int kNumBars = 4 * kStages + 2 * kNSB + 3;
-  static constexpr uint32_t kDataBytes = 2u * kStages * kTileBytes;
+  static constexpr uint32_t kDataBytes = kQBytes + 2u * kStages * kTileBytes;
   static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2)
-    sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmK,
+    sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                           const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using C = KCfg<D>;
   constexpr int NS = C::kStages;
@@ -104,7 +113,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
 
-  const uint32_t sK = base;
+  const uint32_t sQ = base;  // only when !kQInTmem
+  const uint32_t sK = base + C::kQBytes;
   const uint32_t sV = sK + NS * C::kTileBytes;
   const uint32_t sBar = sV + NS * C::kTileBytes;
   auto bKfull = [&](int s) { return sBar + 8u * s; };
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   auto bVempty = [&](int s) { return sBar + 8u * (3 * NS + s); };
   auto bSfull = [&](int b) { return sBar + 8u * (4 * NS + b); };
   auto bPfull = [&](int b) { return sBar + 8u * (4 * NS + NSB + b); };
-  const uint32_t bQready = sBar + 8u * (4 * NS + 2 * NSB);      // Q written to TMEM
+  const uint32_t bQready = sBar + 8u * (4 * NS + 2 * NSB);      // Q in TMEM / smem
   const uint32_t bOdone = sBar + 8u * (4 * NS + 2 * NSB + 1);   // one phase per PV_j
   const uint32_t bOfinal = sBar + 8u * (4 * NS + 2 * NSB + 2);  // single phase: all PVs done
   const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
@@ -134,12 +144,13 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(bSfull(b), 1);
       mbar_init(bPfull(b), 4);  // one arrive per softmax warp
     }
-    mbar_init(bQready, 4);
+    mbar_init(bQready, C::kQInTmem ? 4 : 1);  // 4 softmax warps, or the TMA tx arrive
     mbar_init(bOdone, 1);
     mbar_init(bOfinal, 1);
     mbar_fence_init();
   }
   if (warp == 4 && lane == 0) {
+    if (!C::kQInTmem) tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
   }
@@ -155,6 +166,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint64_t pol_kv = l2_policy_evict_last();
       const int head = int(it.head);
       const uint32_t* ent = p.entries + it.begin;
+      if (!C::kQInTmem) {  // both 64-row Q blocks of the tile, via TMA
+        const uint64_t pol_q = l2_policy_evict_first();
+        mbar_expect_tx(bQready, C::kQBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_3d(sQ + c * C::kQChunk, &tmQ, c * 64, head, int(it.qa) * 64, bQready, pol_q);
+          tma_load_3d(sQ + c * C::kQChunk + 8192, &tmQ, c * 64, head, int(it.qb) * 64, bQready,
+                      pol_q);
+        }
+      }
       auto load_tile = [&](const CUtensorMap* tm, uint32_t dst, uint32_t full, uint32_t j) {
         const int kv = int(__ldg(ent + j) & dbsp_core::kEntryKvMask);
         mbar_expect_tx(full, C::kTileBytes);
@@ -194,7 +215,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint64_t bd =
               smem_desc_sw128(sK + s * C::kTileBytes + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-          mma_ts(dcol, tmem + C::kColQ + kk * 8, bd, kIdescQK, kk > 0 ? 1u : 0u);
+          if constexpr (C::kQInTmem) {
+            mma_ts(dcol, tmem + C::kColQ + kk * 8, bd, kIdescQK, kk > 0 ? 1u : 0u);
+          } else {
+            const uint64_t ad =
+                smem_desc_sw128(sQ + (kk >> 2) * C::kQChunk + (kk & 3) * 32, 16, 1024);
+            mma_ss(dcol, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+          }
         }
         tc_commit(bKempty(s));
         tc_commit(bSfull(int(j % NSB)));
@@ -244,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t lane_off = uint32_t(warp * 32) << 16;
     const uint32_t qblk = upper ? it.qb : it.qa;
     const uint32_t token = qblk * 64u + uint32_t(row & 63);
-    if (count > 0) {
+    if (C::kQInTmem && count > 0) {
       const bool in = token < p.q_tokens;
       const uint4* src = reinterpret_cast<const uint4*>(p.q + (size_t(token) * p.heads + it.head) * D);
 #pragma unroll
