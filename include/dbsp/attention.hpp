@@ -1,0 +1,69 @@
+// The attention call the reference only models: block-
+// sparse softmax(QK^T/sqrt(d))V over the dense 64x64 tiles of a mask set, run
+// by the sm_100a tcgen05 kernel in libdbsp_b200.so.  Device pointers, bf16,
+// token-major [tokens, heads, d], d in {64, 128}; stream-ordered.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "../dbsp_b200.h"
+#include "error.hpp"
+#include "mask.hpp"
+
+namespace dbsp {
+
+struct AttentionArgs {
+  const void* q = nullptr;  // bf16 [q_tokens, heads, d]
+  const void* k = nullptr;  // bf16 [kv_tokens, heads, d]
+  const void* v = nullptr;
+  void* o = nullptr;        // bf16 [q_tokens, heads, d]
+  float* lse = nullptr;     // optional fp32 [heads, q_tokens]
+  uint32_t q_tokens = 0, kv_tokens = 0, heads = 0, head_dim = 0;
+  float softmax_scale = 0.f;  // 0 -> 1/sqrt(d)
+};
+
+// Reusable work list: build once per (mask set, local view), launch many times.
+class AttentionSchedule {
+ public:
+  AttentionSchedule() { detail::check(dbsp_schedule_create(&h_)); }
+  ~AttentionSchedule() { dbsp_schedule_destroy(h_); }
+  AttentionSchedule(const AttentionSchedule&) = delete;
+  AttentionSchedule& operator=(const AttentionSchedule&) = delete;
+
+  // Whole-problem schedule (identity local view).
+  void build(const AttentionMaskSet& set, uint32_t kv_tokens) {
+    detail::MaskView v(set);
+    dbsp_local_view lv{set.num_heads(), nullptr, set.num_q_blocks(), nullptr,
+                       set.num_kv_blocks(), nullptr, kv_tokens};
+    detail::check(dbsp_schedule_build(h_, v.get(), &lv, 1));
+  }
+  // One rank's share: local head / Q-block / KV-block ids in buffer order.
+  void build(const AttentionMaskSet& set, const std::vector<uint32_t>& heads,
+             const std::vector<uint32_t>& q_blocks, const std::vector<uint32_t>& kv_blocks,
+             uint32_t kv_tokens_global) {
+    detail::MaskView v(set);
+    dbsp_local_view lv{uint32_t(heads.size()), heads.data(), uint32_t(q_blocks.size()),
+                       q_blocks.data(), uint32_t(kv_blocks.size()), kv_blocks.data(),
+                       kv_tokens_global};
+    detail::check(dbsp_schedule_build(h_, v.get(), &lv, 1));
+  }
+  void launch(const AttentionArgs& a, void* stream) {
+    const dbsp_attn_args c{a.q, a.k, a.v, a.o, a.lse, nullptr, nullptr, a.q_tokens, a.kv_tokens,
+                           a.heads, a.head_dim, a.softmax_scale, 0, 0};
+    detail::check(dbsp_attention_launch(h_, &c, stream));
+  }
+  dbsp_schedule* handle() const { return h_; }
+
+ private:
+  dbsp_schedule* h_ = nullptr;
+};
+
+inline void sparse_attention(const AttentionMaskSet& set, const AttentionArgs& a, void* stream) {
+  detail::MaskView v(set);
+  const dbsp_attn_args c{a.q, a.k, a.v, a.o, a.lse, nullptr, nullptr, a.q_tokens, a.kv_tokens,
+                         a.heads, a.head_dim, a.softmax_scale, 0, 0};
+  detail::check(dbsp_sparse_attention(v.get(), &c, stream));
+}
+
+}  // namespace dbsp
