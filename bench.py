@@ -64,7 +64,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx),
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
@@ -251,6 +251,8 @@ def run_single(args, wl):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    if args.sp_sim > 1:
+        res["sp_projection"] = sp_projection(q, k, v, masks, args.sp_sim)
     if not args.no_cpu_baseline:
         cb = cpu_attention_baseline(wl, masks, budget_s=args.cpu_budget)
         rp = reference_planner_baseline(wl)
@@ -260,6 +262,38 @@ def run_single(args, wl):
                                        "plan_dual_ms": {s: v["plan_dual_ms"] for s, v in rp["strategies"].items()}}
         res["cpu_baseline"] = cb
     return res
+
+
+def sp_projection(q, k, v, masks, G: int = 8) -> dict:
+    """Every rank's per-period K4 launches of each U x R split run on this one
+    GPU (sp.simulate_on_one_gpu) under the uniform USP plan and the db-SP
+    plan.  Reports the measured attention critical path sum_p max_r t[p][r]
+    (communication excluded), the measured rho_s of kernel times and the
+    plan's rho_s; checks the partitioned output against the one-shot kernel."""
+    import torch
+
+    import paper_2511_23113_b200 as D
+    from paper_2511_23113_b200.attention import sparse_attention
+    from paper_2511_23113_b200.sp import measured_rho, simulate_on_one_gpu
+
+    ref = sparse_attention(q, k, v, masks)
+    out = {}
+    for st in D.enumerate_strategies(G):
+        if st.ulysses > masks.num_heads:
+            continue
+        for name, plan in (("uniform", D.default_plan(masks, st)), ("dbsp", D.plan_dual(masks, st).plan)):
+            o, t = simulate_on_one_gpu(q, k, v, masks, st, plan)
+            crit = float(sum(max(row) for row in t))
+            err = float((o.float() - ref.float()).abs().max())
+            out[f"{st}/{name}"] = {"attn_critical_path_ms": round(crit, 4),
+                                   "rho_s_measured": round(measured_rho(t), 4),
+                                   "rho_s_plan": round(D.imbalance_ratio(D.workload_table(masks, st, plan)), 4),
+                                   "max_abs_vs_single_gpu": round(err, 5)}
+    best_uniform = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("uniform"))
+    best_dbsp = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("dbsp"))
+    return {"gpus_simulated": G, "splits": out, "best_uniform_ms": best_uniform, "best_dbsp_ms": best_dbsp,
+            "speedup_dbsp_vs_best_uniform": round(best_uniform / best_dbsp, 4),
+            "note": "per-rank kernels measured on one B200; communication not included"}
 
 
 def ncu_traffic(workload_name: str):
@@ -313,7 +347,7 @@ def run_reference(args, wl, rank: int) -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="wan")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -322,6 +356,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--ref-budget", type=float, default=4.0)
+    ap.add_argument("--sp-sim", type=int, default=8,
+                    help="N=1 only: simulate every rank of each UxRy split for this many GPUs (0 = off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

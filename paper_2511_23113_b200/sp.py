@@ -1,0 +1,375 @@
+"""Sequence-parallel execution of one block-sparse attention call (the
+execution layer the reference only models: SURVEY.md §2.2 C1-C4, K5).
+
+Home layout: rank g holds token blocks [floor(g*nb/G), floor((g+1)*nb/G)) of
+Q, K, V with all heads, bf16 [tokens, H, d].  A call under strategy UxRy and
+partition plan (head_assignment, q_assignment, kv_assignment) runs on GPU
+g = u*y + r (metrics.hpp:116):
+
+1. one all-G all-to-all(v) (C1 Ulysses head scatter fused with C2, the
+   db-SP balancing moves -- NVSwitch is uniform, so one exchange costs the
+   same as the Ulysses one): GPU (u, r) receives Q blocks {q : q_assign = r}
+   and KV blocks {k : kv_assign = r} for heads {h : head_assign = u};
+2. y ring periods (C3): in period p the GPU holds KV group (r + p) mod y
+   (metrics.hpp:131-132), runs K4 on it in accumulate mode (K5 merge in the
+   epilogue) while the next group travels to it from ring neighbour r+1 over
+   NCCL send/recv on NCCL's stream;
+3. the reverse all-to-all(v) returns O to the home layout.
+
+The same per-rank layout drives three executors: the NCCL one (one process
+per GPU), a single-process simulation that runs every rank's kernels on one
+GPU (for parity and for measured per-rank kernel times, i.e. a measured
+rho_s), and CPU/gloo tests that inject an oracle compute function.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence
+
+import numpy as np
+
+from .planner import AttentionMaskSet, ContractError, ParallelStrategy, PartitionPlan
+
+
+def home_range(rank: int, world: int, nblocks: int):
+    return (rank * nblocks) // world, ((rank + 1) * nblocks) // world
+
+
+@dataclass
+class RankLayout:
+    rank: int
+    u: int
+    r: int
+    heads: np.ndarray                 # global head ids on this GPU (ascending)
+    q_blocks: np.ndarray              # global Q block ids (ascending) -> local Q buffer order
+    kv_groups: List[np.ndarray]       # per ring group g: global KV block ids (ascending)
+    period_groups: List[int] = field(default_factory=list)  # group held in period p
+
+    @property
+    def y(self) -> int:
+        return len(self.kv_groups)
+
+
+def rank_layouts(strategy: ParallelStrategy, plan: PartitionPlan, nq: int, nk: int) -> List[RankLayout]:
+    x, y = strategy.ulysses, strategy.ring
+    ha = np.asarray(plan.head_assignment)
+    qa = np.asarray(plan.q_assignment)
+    ka = np.asarray(plan.kv_assignment)
+    if len(qa) != nq or len(ka) != nk:
+        raise ContractError("plan dimensions do not match the block grid")
+    groups = [np.flatnonzero(ka == g).astype(np.int64) for g in range(y)]
+    out = []
+    for u in range(x):
+        heads = np.flatnonzero(ha == u).astype(np.int64)
+        for r in range(y):
+            out.append(RankLayout(u * y + r, u, r, heads, np.flatnonzero(qa == r).astype(np.int64),
+                                  groups, [(r + p) % y for p in range(y)]))
+    return out
+
+
+@dataclass
+class ExchangePlan:
+    """Token/head index lists of the fused all-to-all(v) for one rank."""
+    # per peer: (home-local token rows to gather for Q, for KV) on the send side
+    send_q_rows: List[np.ndarray]
+    send_kv_rows: List[np.ndarray]
+    send_heads: List[np.ndarray]
+    # per peer: number of Q / KV blocks received (contiguous, peer order)
+    recv_q_blocks: List[int]
+    recv_kv_blocks: List[int]
+
+
+def exchange_plan(rank: int, world: int, layouts: List[RankLayout], nb: int) -> ExchangePlan:
+    lo, hi = home_range(rank, world, nb)
+    me = layouts[rank]
+    sq, skv, sh, rq, rkv = [], [], [], [], []
+    for d in range(world):
+        dst = layouts[d]
+        qb = dst.q_blocks[(dst.q_blocks >= lo) & (dst.q_blocks < hi)]
+        kb = dst.kv_groups[dst.r]
+        kb = kb[(kb >= lo) & (kb < hi)]
+        sq.append(_rows(qb - lo))
+        skv.append(_rows(kb - lo))
+        sh.append(dst.heads)
+        slo, shi = home_range(d, world, nb)
+        rq.append(int(((me.q_blocks >= slo) & (me.q_blocks < shi)).sum()))
+        g = me.kv_groups[me.r]
+        rkv.append(int(((g >= slo) & (g < shi)).sum()))
+    return ExchangePlan(sq, skv, sh, rq, rkv)
+
+
+def _rows(local_blocks: np.ndarray) -> np.ndarray:
+    if len(local_blocks) == 0:
+        return np.zeros(0, np.int64)
+    return (local_blocks[:, None] * 64 + np.arange(64)[None, :]).reshape(-1)
+
+
+# ----------------------------------------------------------------------------- executor
+AttnFn = Callable[..., None]
+"""attn_fn(layout, period, q_local, k_buf, v_buf, out_local, o_acc, lse_acc,
+first: bool, last: bool, kv_blocks) -- computes K4 for one ring period,
+merging into (o_acc, lse_acc) and writing out_local on the last period."""
+
+
+class SPAttention:
+    """One process per GPU.  Torch tensors on `device`; collectives through
+    torch.distributed (NCCL on GPUs, gloo in CPU tests)."""
+
+    def __init__(self, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
+                 tokens: int, head_dim: int, rank: int, world: int, device, attn_fn: AttnFn = None,
+                 group=None):
+        if strategy.gpus() != world:
+            raise ContractError(f"strategy {strategy} needs {strategy.gpus()} ranks, have {world}")
+        if tokens % 64:
+            raise ContractError("the SP path needs a token count that is a multiple of 64")
+        self.masks, self.strategy, self.plan = masks, strategy, plan
+        self.S, self.d, self.rank, self.world = tokens, head_dim, rank, world
+        self.nb = tokens // 64
+        self.device = device
+        self.group = group
+        self.layouts = rank_layouts(strategy, plan, masks.num_q_blocks, masks.num_kv_blocks)
+        self.me = self.layouts[rank]
+        self.xp = exchange_plan(rank, world, self.layouts, self.nb)
+        # reverse exchange: what each peer sends back to me / I send back to each home
+        self.attn_fn = attn_fn or _cuda_attn_fn(masks, self.me, tokens)
+        self._prepare_indices()
+
+    # -- index tensors (host -> device once per plan)
+    def _prepare_indices(self):
+        import torch
+        dev = self.device
+        t = lambda a: torch.as_tensor(np.asarray(a, np.int64), device=dev)
+        self.send_q_rows = [t(a) for a in self.xp.send_q_rows]
+        self.send_kv_rows = [t(a) for a in self.xp.send_kv_rows]
+        self.send_heads = [t(a) for a in self.xp.send_heads]
+        # reverse: my O_local rows per home rank (contiguous slices) and, on the
+        # receiving side, where peer pieces land in my home shard
+        lo, hi = home_range(self.rank, self.world, self.nb)
+        self.o_slices = []
+        off = 0
+        for s in range(self.world):
+            n = self.xp.recv_q_blocks[s]
+            self.o_slices.append((off * 64, (off + n) * 64))
+            off += n
+        self.back_rows, self.back_heads = [], []
+        for s in range(self.world):
+            src = self.layouts[s]
+            qb = src.q_blocks[(src.q_blocks >= lo) & (src.q_blocks < hi)]
+            self.back_rows.append(t(_rows(qb - lo)))
+            self.back_heads.append(t(src.heads))
+
+    def __call__(self, q_home, k_home, v_home, out_home=None):
+        import torch
+        import torch.distributed as dist
+        H = self.masks.num_heads
+        Hu = len(self.me.heads)
+        d = self.d
+        dev = self.device
+        dt = q_home.dtype
+        world, rank = self.world, self.rank
+        nq_loc = len(self.me.q_blocks)
+        group_sizes = [len(g) for g in self.me.kv_groups]
+        max_g = max(group_sizes) if group_sizes else 0
+        q_loc = torch.empty(nq_loc * 64, Hu, d, device=dev, dtype=dt)
+        kbuf = [torch.empty(max(max_g, 1) * 64, Hu, d, device=dev, dtype=dt) for _ in range(2)]
+        vbuf = [torch.empty(max(max_g, 1) * 64, Hu, d, device=dev, dtype=dt) for _ in range(2)]
+
+        # ---- 1. fused Ulysses + balancing all-to-all(v)
+        ops, sends = [], []
+        qoff = kvoff = 0
+        for s in range(world):
+            nq_s, nkv_s = self.xp.recv_q_blocks[s], self.xp.recv_kv_blocks[s]
+            qdst = q_loc[qoff * 64:(qoff + nq_s) * 64]
+            kdst = kbuf[0][kvoff * 64:(kvoff + nkv_s) * 64]
+            vdst = vbuf[0][kvoff * 64:(kvoff + nkv_s) * 64]
+            qoff += nq_s
+            kvoff += nkv_s
+            # what I send to s
+            hq = self.send_heads[s]
+            pq = q_home.index_select(0, self.send_q_rows[s]).index_select(1, hq) if len(self.send_q_rows[s]) else None
+            pk = k_home.index_select(0, self.send_kv_rows[s]).index_select(1, hq) if len(self.send_kv_rows[s]) else None
+            pv = v_home.index_select(0, self.send_kv_rows[s]).index_select(1, hq) if len(self.send_kv_rows[s]) else None
+            if s == rank:
+                if pq is not None:
+                    qdst.copy_(pq)
+                if pk is not None:
+                    kdst.copy_(pk)
+                    vdst.copy_(pv)
+                continue
+            # zero-size pieces are skipped on both sides (sizes are derived from
+            # the same plan on sender and receiver, so the op lists match)
+            for buf, dst in ((pq, qdst), (pk, kdst), (pv, vdst)):
+                if buf is not None and buf.numel():
+                    buf = buf.contiguous()
+                    sends.append(buf)
+                    ops.append(dist.P2POp(dist.isend, buf, s, group=self.group))
+                if dst.numel():
+                    ops.append(dist.P2POp(dist.irecv, dst, s, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+        # ---- 2. ring periods: compute on the held group while the next arrives
+        y = self.strategy.ring
+        o_loc = torch.empty(nq_loc * 64, Hu, d, device=dev, dtype=dt)
+        o_acc = torch.empty(nq_loc * 64, Hu, d, device=dev, dtype=torch.float32) if y > 1 else None
+        lse_acc = torch.empty(Hu, nq_loc * 64, device=dev, dtype=torch.float32) if y > 1 else None
+        cur = 0
+        nxt_rank = self.me.u * y + (self.me.r + 1) % y
+        prv_rank = self.me.u * y + (self.me.r - 1) % y
+        for p in range(y):
+            g = self.me.period_groups[p]
+            n = group_sizes[g]
+            reqs = []
+            if p < y - 1:
+                gn = self.me.period_groups[p + 1]
+                nn = group_sizes[gn]
+                ops = []
+                if n and Hu:
+                    ops += [dist.P2POp(dist.isend, kbuf[cur][:n * 64], prv_rank, group=self.group),
+                            dist.P2POp(dist.isend, vbuf[cur][:n * 64], prv_rank, group=self.group)]
+                if nn and Hu:
+                    ops += [dist.P2POp(dist.irecv, kbuf[1 - cur][:nn * 64], nxt_rank, group=self.group),
+                            dist.P2POp(dist.irecv, vbuf[1 - cur][:nn * 64], nxt_rank, group=self.group)]
+                if ops:
+                    reqs = dist.batch_isend_irecv(ops)
+            self.attn_fn(self.me, p, q_loc, kbuf[cur][:n * 64], vbuf[cur][:n * 64], o_loc, o_acc, lse_acc,
+                         p == 0, p == y - 1, self.me.kv_groups[g])
+            for w in reqs:
+                w.wait()
+            cur = 1 - cur
+
+        # ---- 3. reverse all-to-all(v): O back to the home layout
+        T_home = q_home.shape[0]
+        if out_home is None:
+            out_home = torch.empty(T_home, H, d, device=dev, dtype=dt)
+        ops, recvs = [], []
+        for s in range(world):
+            a, b = self.o_slices[s]
+            rows, heads = self.back_rows[s], self.back_heads[s]
+            if s == rank:
+                if b > a:
+                    out_home[rows[:, None], heads[None, :]] = o_loc[a:b]
+                continue
+            if b > a and Hu:
+                ops.append(dist.P2POp(dist.isend, o_loc[a:b].contiguous(), s, group=self.group))
+            if len(rows) and len(heads):
+                buf = torch.empty(len(rows), len(heads), d, device=dev, dtype=dt)
+                recvs.append((buf, rows, heads))
+                ops.append(dist.P2POp(dist.irecv, buf, s, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for buf, rows, heads in recvs:
+            out_home[rows[:, None], heads[None, :]] = buf
+        return out_home
+
+
+def _cuda_attn_fn(masks: AttentionMaskSet, me: RankLayout, tokens: int) -> AttnFn:
+    """K4 per ring period on the local buffers; schedules built once per plan."""
+    from .attention import AttentionSchedule, accum_init
+
+    scheds: Dict[int, AttentionSchedule] = {}
+
+    def fn(layout, period, q_loc, k_buf, v_buf, out_loc, o_acc, lse_acc, first, last, kv_blocks):
+        if len(layout.q_blocks) == 0 or len(layout.heads) == 0:
+            return
+        g = layout.period_groups[period]
+        if g not in scheds:
+            if len(kv_blocks) == 0:
+                scheds[g] = None
+            else:
+                scheds[g] = AttentionSchedule().build(masks, head_ids=layout.heads, q_block_ids=layout.q_blocks,
+                                                      kv_block_ids=kv_blocks, kv_tokens_global=tokens)
+        sc = scheds[g]
+        y = layout.y
+        if y == 1:
+            if sc is None:
+                out_loc.zero_()
+            else:
+                sc.launch(q_loc, k_buf, v_buf, out_loc)
+            return
+        if first:
+            accum_init(o_acc, lse_acc)
+        if sc is not None:
+            sc.launch(q_loc, k_buf, v_buf, out_loc, o_accum=o_acc, lse_accum=lse_acc, accumulate=True,
+                      finalize=last)
+        elif last:
+            out_loc.copy_(o_acc.to(out_loc.dtype))
+
+    return fn
+
+
+# ----------------------------------------------------------------------------- single-GPU simulation
+def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
+                        time_kernels: bool = True, reps: int = 3):
+    """Run every rank's per-period kernels of UxRy on ONE GPU (no exchange:
+    the local buffers are gathered from the global tensors), merge exactly as
+    the distributed path does, and time each (rank, period) launch with CUDA
+    events.  Returns (out [S,H,d], times_ms[period][rank])."""
+    import torch
+    from .attention import AttentionSchedule, accum_init
+
+    S, H, d = q.shape
+    nb = S // 64
+    layouts = rank_layouts(strategy, plan, masks.num_q_blocks, masks.num_kv_blocks)
+    y = strategy.ring
+    out = torch.zeros_like(q)
+    times = [[0.0] * len(layouts) for _ in range(y)]
+    for lay in layouts:
+        if len(lay.heads) == 0 or len(lay.q_blocks) == 0:
+            continue
+        hs = torch.as_tensor(lay.heads, device=q.device)
+        rows = torch.as_tensor(_rows(lay.q_blocks), device=q.device)
+        q_loc = q.index_select(0, rows).index_select(1, hs).contiguous()
+        o_loc = torch.empty_like(q_loc)
+        o_acc = torch.empty(q_loc.shape, device=q.device, dtype=torch.float32)
+        lse_acc = torch.empty(len(lay.heads), q_loc.shape[0], device=q.device, dtype=torch.float32)
+        accum_init(o_acc, lse_acc)
+        for p in range(y):
+            g = lay.period_groups[p]
+            kvb = lay.kv_groups[g]
+            if len(kvb) == 0:
+                if p == y - 1:
+                    o_loc.copy_(o_acc.to(o_loc.dtype)) if y > 1 else o_loc.zero_()
+                continue
+            kr = torch.as_tensor(_rows(kvb), device=q.device)
+            k_loc = k.index_select(0, kr).index_select(1, hs).contiguous()
+            v_loc = v.index_select(0, kr).index_select(1, hs).contiguous()
+            sc = AttentionSchedule().build(masks, head_ids=lay.heads, q_block_ids=lay.q_blocks,
+                                           kv_block_ids=kvb, kv_tokens_global=S)
+            sc.upload()
+            if time_kernels:
+                # time on a scratch accumulator so the merge below is not disturbed
+                oa = torch.empty_like(o_acc)
+                la = torch.empty_like(lse_acc)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                best = float("inf")
+                for _ in range(reps):
+                    accum_init(oa, la)
+                    ev[0].record()
+                    if y == 1:
+                        sc.launch(q_loc, k_loc, v_loc, o_loc)
+                    else:
+                        sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=oa, lse_accum=la, accumulate=True)
+                    ev[1].record()
+                    torch.cuda.synchronize()
+                    best = min(best, ev[0].elapsed_time(ev[1]))
+                times[p][lay.rank] = best
+            if y == 1:
+                sc.launch(q_loc, k_loc, v_loc, o_loc)
+            else:
+                sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=o_acc, lse_accum=lse_acc, accumulate=True,
+                          finalize=(p == y - 1))
+        out[rows[:, None], hs[None, :]] = o_loc
+    torch.cuda.synchronize()
+    return out, times
+
+
+def measured_rho(times: Sequence[Sequence[float]]) -> float:
+    """rho_s of measured per-(period, rank) kernel times (Eq. 1 on seconds)."""
+    t = np.asarray(times, dtype=np.float64)
+    total = t.sum()
+    if total == 0:
+        return 1.0
+    return float(t.max(axis=1).sum() * t.shape[1] / total)
