@@ -301,10 +301,14 @@ typedef struct dbsp_local_view {
 
 int dbsp_schedule_create(dbsp_schedule** out);
 void dbsp_schedule_destroy(dbsp_schedule* sched);
-/* Builds the work list for `view` against `set` (host).  pair_q != 0 packs
- * two Q blocks per 128-row tile (the tcgen05 M=128 path). */
+/* Schedule flags.  PAIR_Q packs two Q blocks per 128-row tile (the tcgen05
+ * M=128 path).  Launch order is heaviest-first; GLOBAL_LPT orders across
+ * heads, HEAD_ORDER within each head (K/V of concurrently running CTAs stays
+ * L2-resident); with neither, small local problems get GLOBAL_LPT. */
+enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4 };
+/* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
-                        const dbsp_local_view* view, int32_t pair_q);
+                        const dbsp_local_view* view, int32_t flags);
 /* Stats of the last build: items, entries (tile visits), dense tiles. */
 int dbsp_schedule_stats(const dbsp_schedule* sched, uint64_t* items, uint64_t* tile_visits,
                         uint64_t* dense_tiles);

@@ -194,7 +194,7 @@ int dbsp_schedule_create(dbsp_schedule** out) {
 void dbsp_schedule_destroy(dbsp_schedule* s) { delete s; }
 
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
-                        const dbsp_local_view* view, int32_t pair_q) {
+                        const dbsp_local_view* view, int32_t flags) {
   return guard([&] {
     if (!sched || !set) fail(kContract, "null schedule or mask set");
     const MaskView m =
@@ -213,7 +213,7 @@ int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
       lv.q_blocks = m.nq;
       lv.kv_blocks = m.nk;
     }
-    build_schedule(m, lv, pair_q != 0, sched->host);
+    build_schedule(m, lv, uint32_t(flags), sched->host);
     sched->dirty = true;
   });
 }

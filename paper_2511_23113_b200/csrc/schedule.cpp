@@ -7,7 +7,11 @@
 
 namespace dbsp_core {
 
-void build_schedule(const MaskView& m, const LocalView& v, bool pair_q, Schedule& out) {
+void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out) {
+  const bool pair_q = (flags & kSchedPairQ) != 0;
+  bool global_lpt = (flags & kSchedGlobalLpt) != 0;
+  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto: K/V of <= 8 heads x 512 blocks
+    global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
   if (v.heads == 0 || v.q_blocks == 0 || v.kv_blocks == 0)
     fail(kConfig, "local view dimensions must be positive");
   if (v.kv_blocks > kEntryKvMask) fail(kConfig, "too many local KV blocks");
@@ -74,8 +78,13 @@ void build_schedule(const MaskView& m, const LocalView& v, bool pair_q, Schedule
   }
   std::vector<uint32_t> order(raw.size());
   std::iota(order.begin(), order.end(), 0u);
+  // Heaviest-first (LPT) launch order.  The hardware hands CTAs to free SM
+  // slots in blockIdx order, so this is a dynamic LPT schedule.  For large
+  // problems the order is per head so concurrently running CTAs share a
+  // head's K/V in L2; when the whole local K/V fits comfortably in L2 the
+  // order is global, which removes the per-head tails.
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
-    if (raw[x].it.head != raw[y].it.head) return raw[x].it.head < raw[y].it.head;
+    if (!global_lpt && raw[x].it.head != raw[y].it.head) return raw[x].it.head < raw[y].it.head;
     return raw[x].it.count > raw[y].it.count;
   });
   out.items.clear();

@@ -49,9 +49,12 @@ struct Schedule {
   uint32_t max_head = 0, max_q_block = 0, max_kv_block = 0;  // bounds checked at launch
 };
 
-// Builds items ordered by local head, heaviest first within a head (keeps
-// the K/V working set of concurrently running CTAs L2-resident while the
-// heaviest tiles start first).
-void build_schedule(const MaskView& m, const LocalView& v, bool pair_q, Schedule& out);
+// Schedule flags (dbsp_schedule_build's `flags`).
+constexpr uint32_t kSchedPairQ = 1;      // two Q blocks per 128-row tile
+constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all heads
+constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
+
+// Builds the work items in LPT launch order (see schedule.cpp).
+void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out);
 
 }  // namespace dbsp_core
