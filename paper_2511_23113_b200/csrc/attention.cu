@@ -11,7 +11,10 @@
 #include <string>
 
 #include "../../include/dbsp_b200.h"
+#include <cstdlib>
+
 #include "attn_kernel.cuh"
+#include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
 #include "core.hpp"
 #include "schedule.hpp"
@@ -114,6 +117,29 @@ void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap
   cuda_check(attr_err, "cudaFuncSetAttribute");
   dbsp_dev::sparse_attn_fwd_kernel<D><<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd launch");
+}
+
+void launch_wide(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm,
+                 uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::WideCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_wide_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(wide)");
+  dbsp_dev::sparse_attn_fwd_wide_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_wide launch");
+}
+
+// d=128 kernel choice: the 128-key-step variant unless DBSP_K4_NARROW=1.
+bool use_wide() {
+  static const bool wide = [] {
+    const char* e = std::getenv("DBSP_K4_NARROW");
+    return !(e && e[0] == '1');
+  }();
+  return wide;
 }
 
 unsigned long long* g_trace = nullptr;
@@ -281,7 +307,9 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
-    if (a->head_dim == 128)
+    if (a->head_dim == 128 && use_wide())
+      launch_wide(tk, tv, prm, uint32_t(h.items.size()), stream);
+    else if (a->head_dim == 128)
       launch_kernel<128>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
     else
       launch_kernel<64>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
