@@ -158,6 +158,14 @@ int dbsp_density(const dbsp_mask_set* set, double* out);
 /* mix_seed (rng.hpp:37-40). */
 uint64_t dbsp_mix_seed(uint64_t base, uint64_t a, uint64_t b);
 
+/* DBSPMSK1 mask files (mask_io.hpp:131-207): atomic save; load in two calls
+ * (header for the dimensions, then words sized H*Nq*ceil(Nk/64)).  Errors:
+ * DBSP_ERR_IO for filesystem failures, DBSP_ERR_PARSE with the byte offset. */
+int dbsp_save_mask_set(const dbsp_mask_set* set, const char* path);
+int dbsp_load_mask_set_header(const char* path, uint32_t* heads, uint32_t* q_blocks,
+                              uint32_t* kv_blocks, uint32_t* block_size);
+int dbsp_load_mask_set(const char* path, uint64_t* words_out);
+
 /* ------------------------------------------------------------------------ */
 /* Strategy / plan / rho_s (metrics.hpp)                                     */
 

@@ -14,7 +14,8 @@ from .planner import (  # noqa: F401
     PlanOutcome, ProfileSample, SearchSpaceError, Selection, SelectorState, StrategyPrediction,
     WorkloadTable, biased_greedy, blocks_per_head, brute_force_blocks, brute_force_heads,
     default_plan, density, enumerate_strategies, exchange_volume, fit_profile,
-    generate_mask_set, head_level_imbalance, imbalance_ratio, kInfiniteReward, mix_seed,
+    generate_mask_set, head_level_imbalance, imbalance_ratio, kInfiniteReward, load_mask_set,
+    mix_seed, save_mask_set,
     parse_strategy, partition_blocks, partition_heads, perturb_mask_set, plan_dual,
     predict_all, predict_from_inputs, predict_latency, select, summed_grid, total_blocks,
     validate_plan, workload_table)

@@ -111,6 +111,9 @@ _SIGS = {
     "dbsp_total_blocks": (C.c_int, [P(MaskSetT), P(u64)]),
     "dbsp_blocks_per_head": (C.c_int, [P(MaskSetT), P(u64)]),
     "dbsp_density": (C.c_int, [P(MaskSetT), P(f64)]),
+    "dbsp_save_mask_set": (C.c_int, [P(MaskSetT), C.c_char_p]),
+    "dbsp_load_mask_set_header": (C.c_int, [C.c_char_p, P(u32), P(u32), P(u32), P(u32)]),
+    "dbsp_load_mask_set": (C.c_int, [C.c_char_p, P(u64)]),
     "dbsp_enumerate_strategies": (C.c_int, [u32, P(StrategyT), P(u32)]),
     "dbsp_validate_plan": (C.c_int, [P(MaskSetT), StrategyT, P(PlanT)]),
     "dbsp_default_plan": (C.c_int, [P(MaskSetT), StrategyT, P(PlanT)]),

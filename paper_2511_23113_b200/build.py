@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "dbsp_b200"
 LIB = PKG / "libdbsp_b200.so"
 
-CXX_SOURCES = ["planner_core.cpp", "schedule.cpp", "capi.cpp"]
+CXX_SOURCES = ["planner_core.cpp", "schedule.cpp", "capi.cpp", "mask_io.cpp"]
 CU_SOURCES = ["attention.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 

@@ -196,6 +196,59 @@ def perturb_mask_set(mset: AttentionMaskSet, flip_rate: float, seed: int) -> Att
     return AttentionMaskSet(out, mset.nk, mset.block_size)
 
 
+def save_mask_set(mset: AttentionMaskSet, path) -> None:
+    """DBSPMSK1 binary file, written atomically (mask_io.hpp:131-147)."""
+    check(L.lib().dbsp_save_mask_set(C.byref(mset.c()), str(path).encode()))
+
+
+def load_mask_set(path) -> AttentionMaskSet:
+    """DBSPMSK1 binary file, or the JSON hex sidecar accepted for fixtures
+    (mask_io.hpp:80-127,149-207)."""
+    p = str(path)
+    try:
+        with open(p, "rb") as f:
+            head = f.read(64)
+    except OSError:
+        raise IoError(f"cannot open '{p}'") from None
+    if not head.startswith(b"DBSPMSK1") and head.lstrip()[:1] == b"{":
+        return _mask_set_from_sidecar(p)
+    dims = [C.c_uint32() for _ in range(4)]
+    check(L.lib().dbsp_load_mask_set_header(p.encode(), *[C.byref(d) for d in dims]))
+    H, nq, nk, bs = (d.value for d in dims)
+    words = np.zeros((H, nq, (nk + 63) // 64), np.uint64)
+    check(L.lib().dbsp_load_mask_set(p.encode(), _u64p(words)))
+    return AttentionMaskSet(words, nk, bs)
+
+
+def _mask_set_from_sidecar(path: str) -> AttentionMaskSet:
+    import json
+    try:
+        with open(path) as f:
+            j = json.load(f)
+    except json.JSONDecodeError as e:
+        raise ParseError(f"{path}: invalid JSON sidecar: {e}") from None
+    try:
+        H, nq, nk, bs = (int(j[k]) for k in ("heads", "q_blocks", "kv_blocks", "block_size"))
+        rows = j["rows"]
+    except KeyError as e:
+        raise ParseError(f"{path}: sidecar is missing a required key: {e}") from None
+    if min(H, nq, nk, bs) <= 0:
+        raise ParseError(f"{path}: sidecar dimensions must be positive")
+    if len(rows) != H * nq:
+        raise ParseError(f"{path}: sidecar needs heads*q_blocks row strings, got {len(rows)}")
+    nbytes = (nk + 7) // 8
+    dense = np.zeros((H * nq, nbytes * 8), bool)
+    for r, hx in enumerate(rows):
+        if len(hx) != 2 * nbytes:
+            raise ParseError(f"{path}: row {r} needs {2 * nbytes} hex chars")
+        try:
+            b = bytes.fromhex(hx)
+        except ValueError:
+            raise ParseError(f"{path}: row {r} has a non-hex character") from None
+        dense[r] = np.unpackbits(np.frombuffer(b, np.uint8), bitorder="little").astype(bool)
+    return AttentionMaskSet.from_dense(dense[:, :nk].reshape(H, nq, nk), bs)
+
+
 def mix_seed(base: int, a: int, b: int = 0) -> int:
     m = 0xFFFFFFFFFFFFFFFF
     return int(L.lib().dbsp_mix_seed(base & m, a & m, b & m))
