@@ -149,6 +149,34 @@ def test_partitioned_execution_matches_one_shot(strategy):
         assert float((out.float() - full.float()).abs().max()) < 1e-2
 
 
+def test_nccl_executor_single_rank():
+    # The NCCL-backed executor (the N>1 bench leg) on a 1-rank group: device
+    # index tensors, buffers and the K4 launch path through SPAttention.
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2511_23113_b200.sp import SPAttention
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        H, S, d = 4, 2048, 128
+        nb = S // 64
+        masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.2, 0.5, 1.0, 3))
+        q, k, v = (t.cuda() for t in make_qkv(S, H, d, 5))
+        st = D.ParallelStrategy(1, 1)
+        sp = SPAttention(masks, st, D.plan_dual(masks, st).plan, S, d, 0, 1, torch.device("cuda"))
+        out = sp(q, k, v)
+        ref = sparse_attention(q, k, v, masks)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_mask_stats_device_exact():
     m = D.generate_mask_set(D.GeneratorSpec(40, 512, 512, 64, "clustered", 0.15, 0.45, 1.0, 1))
     words = torch.from_numpy(m.words.view(np.int64)).cuda()
