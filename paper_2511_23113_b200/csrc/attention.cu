@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "attn_kernel.cuh"
+#include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
 #include "core.hpp"
@@ -131,6 +132,31 @@ void launch_wide(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::Att
   cuda_check(attr_err, "cudaFuncSetAttribute(wide)");
   dbsp_dev::sparse_attn_fwd_wide_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_wide launch");
+}
+
+template <int D>
+void launch_split(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::KCfg<D>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_split_kernel<D>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(split)");
+  dbsp_dev::sparse_attn_fwd_split_kernel<D>
+      <<<items, dbsp_dev::kThreadsSplit, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_split launch");
+}
+
+// Softmax split across 8 warps (attn_kernel_split.cuh) unless DBSP_K4_SPLIT=0.
+bool use_split() {
+  static const bool split = [] {
+    const char* e = std::getenv("DBSP_K4_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return split;
 }
 
 // d=128 kernel choice.  The 128-key-step variant (one CTA/SM) measured 6.96 ms
@@ -310,8 +336,13 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
+    const uint32_t n_items = uint32_t(h.items.size());
     if (a->head_dim == 128 && use_wide())
-      launch_wide(tk, tv, prm, uint32_t(h.items.size()), stream);
+      launch_wide(tk, tv, prm, n_items, stream);
+    else if (use_split() && a->head_dim == 128)
+      launch_split<128>(tq, tk, tv, prm, n_items, stream);
+    else if (use_split())
+      launch_split<64>(tq, tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128)
       launch_kernel<128>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
     else
