@@ -251,6 +251,7 @@ def run_single(args, wl):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    res["planner"] = planner_timing(masks)
     if args.sp_sim > 1:
         res["sp_projection"] = sp_projection(q, k, v, masks, args.sp_sim)
     if not args.no_cpu_baseline:
@@ -262,6 +263,22 @@ def run_single(args, wl):
                                        "plan_dual_ms": {s: v["plan_dual_ms"] for s, v in rp["strategies"].items()}}
         res["cpu_baseline"] = cb
     return res
+
+
+def planner_timing(masks, G: int = 8, reps: int = 5) -> dict:
+    """Our host planner on the bench masks: select() over the G-GPU strategies
+    (fresh SelectorState per call, as ref_bench times the reference)."""
+    import paper_2511_23113_b200 as D
+    from paper_2511_23113_b200.sp_bench import load_profile
+    prof = load_profile()
+    D.select(0, masks, prof, D.PlannerConfig(), D.SelectorState(G))
+    t0 = time.perf_counter()
+    for i in range(reps):
+        sel = D.select(i, masks, prof, D.PlannerConfig(), D.SelectorState(G))
+    ms = (time.perf_counter() - t0) / reps * 1e3
+    return {"select_ms_per_call": round(ms, 3), "gpus_planned": G, "selected": str(sel.strategy),
+            "rho_s_post": round(sel.outcome.rho_post, 4), "profile": "b200_nominal.json",
+            "threads": os.cpu_count()}
 
 
 def sp_projection(q, k, v, masks, G: int = 8) -> dict:

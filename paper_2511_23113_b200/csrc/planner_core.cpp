@@ -7,8 +7,10 @@
 #include <algorithm>
 #include <bit>
 #include <cmath>
+#include <exception>
 #include <limits>
 #include <numeric>
+#include <thread>
 #include <utility>
 
 namespace dbsp_core {
@@ -16,6 +18,29 @@ namespace dbsp_core {
 namespace {
 
 std::string str(uint64_t v) { return std::to_string(v); }
+
+// Splits [0, n) into contiguous chunks over up to `threads` std::threads; the
+// body gets (chunk index, begin, end).  Integer partial results are merged by
+// the caller in chunk order, so results never depend on the thread count.
+template <class F>
+void parallel_chunks(size_t n, size_t threads, F&& body) {
+  threads = std::max<size_t>(1, std::min(threads, n));
+  if (threads == 1) {
+    body(size_t(0), size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < threads; ++t)
+    pool.emplace_back([&, t] { body(t, n * t / threads, n * (t + 1) / threads); });
+  body(size_t(0), size_t(0), n / threads);
+  for (std::thread& th : pool) th.join();
+}
+
+size_t planner_threads(uint64_t work_words) {
+  if (work_words < (uint64_t(1) << 16)) return 1;  // small sets: threads cost more than they save
+  const unsigned hw = std::thread::hardware_concurrency();
+  return std::min<size_t>(hw ? hw : 1, 8);
+}
 
 }  // namespace
 
@@ -76,34 +101,45 @@ MaskStats mask_stats(const MaskView& m, bool marginals) {
   st.have_marginals = true;
   st.row_weights.assign(m.nq, 0);
   st.col_weights.assign(m.nk, 0);
-  const uint64_t rows = uint64_t(m.H) * m.nq;
-  const int planes = std::max(1, int(std::bit_width(rows)));
   const size_t wpr = m.wpr;
-  std::vector<uint64_t> plane(size_t(planes) * wpr, 0);
-  for (uint32_t h = 0; h < m.H; ++h) {
-    for (uint32_t q = 0; q < m.nq; ++q) {
-      const uint64_t* r = m.row(h, q);
-      uint64_t rc = 0;
-      for (size_t w = 0; w < wpr; ++w) {
-        const uint64_t word = r[w];
-        rc += uint64_t(std::popcount(word));
-        uint64_t carry = word;
-        for (int p = 0; carry; ++p) {
-          uint64_t& cell = plane[size_t(p) * wpr + w];
-          const uint64_t t = cell & carry;
-          cell ^= carry;
-          carry = t;
+  const size_t T = planner_threads(uint64_t(m.H) * m.nq * wpr);
+  std::vector<std::vector<uint64_t>> rows_part(T, std::vector<uint64_t>(m.nq, 0));
+  std::vector<std::vector<uint64_t>> cols_part(T, std::vector<uint64_t>(m.nk, 0));
+  parallel_chunks(m.H, T, [&](size_t t, size_t h0, size_t h1) {
+    const uint64_t rows = uint64_t(h1 - h0) * m.nq;
+    const int planes = std::max(1, int(std::bit_width(rows)));
+    std::vector<uint64_t> plane(size_t(planes) * wpr, 0);
+    std::vector<uint64_t>& rw = rows_part[t];
+    for (size_t h = h0; h < h1; ++h) {
+      for (uint32_t q = 0; q < m.nq; ++q) {
+        const uint64_t* r = m.row(uint32_t(h), q);
+        uint64_t rc = 0;
+        for (size_t w = 0; w < wpr; ++w) {
+          const uint64_t word = r[w];
+          rc += uint64_t(std::popcount(word));
+          uint64_t carry = word;  // bit-sliced vertical counter, carry-save increment
+          for (int p = 0; carry; ++p) {
+            uint64_t& cell = plane[size_t(p) * wpr + w];
+            const uint64_t c = cell & carry;
+            cell ^= carry;
+            carry = c;
+          }
         }
+        rw[q] += rc;
       }
-      st.row_weights[q] += rc;
     }
-  }
-  for (uint32_t k = 0; k < m.nk; ++k) {
-    const size_t w = k / 64;
-    const unsigned b = k % 64;
-    uint64_t v = 0;
-    for (int p = 0; p < planes; ++p) v |= ((plane[size_t(p) * wpr + w] >> b) & 1ull) << p;
-    st.col_weights[k] = v;
+    std::vector<uint64_t>& cw = cols_part[t];
+    for (uint32_t k = 0; k < m.nk; ++k) {
+      const size_t w = k / 64;
+      const unsigned b = k % 64;
+      uint64_t v = 0;
+      for (int p = 0; p < planes; ++p) v |= ((plane[size_t(p) * wpr + w] >> b) & 1ull) << p;
+      cw[k] = v;
+    }
+  });
+  for (size_t t = 0; t < T; ++t) {
+    for (uint32_t q = 0; q < m.nq; ++q) st.row_weights[q] += rows_part[t][q];
+    for (uint32_t k = 0; k < m.nk; ++k) st.col_weights[k] += cols_part[t][k];
   }
   return st;
 }
@@ -283,21 +319,27 @@ Table workload_table(const MaskView& m, Strategy s, const uint32_t* head, const 
   const size_t wpr = m.wpr;
   std::vector<uint64_t> group(size_t(y) * wpr, 0);
   for (uint32_t k = 0; k < m.nk; ++k) group[size_t(kv[k]) * wpr + k / 64] |= 1ull << (k % 64);
-  std::vector<uint64_t> per_group(y);
-  for (uint32_t h = 0; h < m.H; ++h) {
-    const uint32_t u = head[h];
-    for (uint32_t qb = 0; qb < m.nq; ++qb) {
-      const uint64_t* r = m.row(h, qb);
-      const uint32_t rr = q[qb];
-      const uint32_t gpu = u * y + rr;
-      for (uint32_t g = 0; g < y; ++g) {
-        const uint64_t* gb = group.data() + size_t(g) * wpr;
-        uint64_t c = 0;
-        for (size_t w = 0; w < wpr; ++w) c += uint64_t(std::popcount(r[w] & gb[w]));
-        t.counts[size_t((g + y - rr) % y) * t.gpus + gpu] += c;
+  const size_t T = planner_threads(uint64_t(m.H) * m.nq * wpr * y / 4);
+  std::vector<std::vector<uint64_t>> part(T, std::vector<uint64_t>(t.counts.size(), 0));
+  parallel_chunks(m.H, T, [&](size_t ti, size_t h0, size_t h1) {
+    std::vector<uint64_t>& cnt = part[ti];
+    for (size_t h = h0; h < h1; ++h) {
+      const uint32_t u = head[h];
+      for (uint32_t qb = 0; qb < m.nq; ++qb) {
+        const uint64_t* r = m.row(uint32_t(h), qb);
+        const uint32_t rr = q[qb];
+        const uint32_t gpu = u * y + rr;
+        for (uint32_t g = 0; g < y; ++g) {
+          const uint64_t* gb = group.data() + size_t(g) * wpr;
+          uint64_t c = 0;
+          for (size_t w = 0; w < wpr; ++w) c += uint64_t(std::popcount(r[w] & gb[w]));
+          cnt[size_t((g + y - rr) % y) * t.gpus + gpu] += c;
+        }
       }
     }
-  }
+  });
+  for (const auto& cnt : part)
+    for (size_t i = 0; i < cnt.size(); ++i) t.counts[i] += cnt[i];
   return t;
 }
 
@@ -751,19 +793,41 @@ std::vector<Prediction> predict_all(const MaskView& m, const Profile& p, uint32_
   for (Strategy s : all)
     if (s.x <= m.H && s.y > 1 && s.y <= std::min(m.nq, m.nk)) ring = true;
   const MaskStats st = mask_stats(m, ring);
-  std::vector<Prediction> out;
-  for (Strategy s : all) {
-    if (s.x > m.H) continue;
-    if (s.y > std::min(m.nq, m.nk)) continue;
-    const auto it = prev.find(s);
-    Prediction pr;
-    pr.strategy = s;
-    pr.outcome = plan_dual(m, s, cfg, it != prev.end() ? &it->second : nullptr, &st);
-    pr.latency = predict_latency(m, s, pr.outcome.plan, p, false, &st, &pr.outcome.rho_post);
-    out.push_back(std::move(pr));
-  }
-  if (out.empty())
+  std::vector<Strategy> feasible;
+  for (Strategy s : all)
+    if (s.x <= m.H && s.y <= std::min(m.nq, m.nk)) feasible.push_back(s);
+  if (feasible.empty())
     fail(kConfig, "no feasible strategy for " + str(gpus) + " GPUs on this mask shape");
+  // Strategies are independent (each reads the shared, immutable MaskStats),
+  // so they are planned on parallel threads; results land in enumeration
+  // order, so the outcome is identical to the sequential loop.
+  std::vector<Prediction> out(feasible.size());
+  std::vector<std::exception_ptr> errs(feasible.size());
+  auto work = [&](size_t i) {
+    try {
+      const Strategy s = feasible[i];
+      const auto it = prev.find(s);
+      Prediction pr;
+      pr.strategy = s;
+      pr.outcome = plan_dual(m, s, cfg, it != prev.end() ? &it->second : nullptr, &st);
+      pr.latency = predict_latency(m, s, pr.outcome.plan, p, false, &st, &pr.outcome.rho_post);
+      out[i] = std::move(pr);
+    } catch (...) {
+      errs[i] = std::current_exception();
+    }
+  };
+  const bool threaded = feasible.size() > 1 && uint64_t(m.H) * m.nq * m.wpr >= 4096 &&
+                        std::thread::hardware_concurrency() > 1;
+  if (threaded) {
+    std::vector<std::thread> pool;
+    for (size_t i = 1; i < feasible.size(); ++i) pool.emplace_back(work, i);
+    work(0);
+    for (std::thread& t : pool) t.join();
+  } else {
+    for (size_t i = 0; i < feasible.size(); ++i) work(i);
+  }
+  for (const std::exception_ptr& e : errs)  // first error in enumeration order wins
+    if (e) std::rethrow_exception(e);
   return out;
 }
 

@@ -47,9 +47,14 @@ WORKLOADS = {
     # A: CPU-ref toy (BASELINE configs[0]).
     "toy": Workload("toy-A", 8, 64, 4096, "random", 0.5, 0.5, 1, 4,
                     "8 heads, 4096 tokens, d=64, 50% random, simulated SP=4 (U2R2)"),
-    # B: CogVideoX-5B-shaped layer (configs[1]); PARO densities 0.586 / 0.317.
-    "cogvideox": Workload("cogvideox-5b-B", 48, 64, 17792, "clustered", 0.317, 0.317, 1, 8,
-                          "48 heads, d=64, 278 blocks, clustered mean 0.317"),
+    # B: CogVideoX-5B-shaped layer (configs[1]); PARO mean density 0.317
+    # with a per-head ramp 0.15-0.484: real PARO/Sparge masks
+    # differ per head (the reference reports rho_s 1.45 for Ulysses on
+    # CogVideoX1.5), a constant density would hide that.
+    "cogvideox": Workload("cogvideox-5b-B", 48, 64, 17792, "clustered", 0.15, 0.484, 1, 8,
+                          "48 heads, d=64, 278 blocks, clustered ramp 0.15-0.484 (mean 0.317)"),
+    "cogvideox-flat": Workload("cogvideox-5b-B-flat", 48, 64, 17792, "clustered", 0.317, 0.317, 1, 8,
+                               "48 heads, d=64, 278 blocks, every head at density 0.317"),
     # C: Wan2.1-T2V-14B 480p layer (configs[2]) -- the north-star workload.
     "wan": Workload("wan2.1-14b-480p-C", 40, 128, 32768, "clustered", 0.15, 0.45, 1, 8,
                     "40 heads, d=128, 512 blocks, clustered 0.15-0.45 (mean 0.30)"),
