@@ -317,6 +317,15 @@ enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER =
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
                         const dbsp_local_view* view, int32_t flags);
+/* K2 on the device: the same work list built from DEVICE mask words
+ * [heads][q_blocks][ceil(kv_blocks/64)] on `stream` (no host pass over the
+ * masks, no upload).  `view` holds host arrays (small); NULL = identity. */
+int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, uint32_t heads,
+                               uint32_t q_blocks, uint32_t kv_blocks,
+                               const dbsp_local_view* view, int32_t flags, void* stream);
+/* Copies the built list to host (32-byte items, u32 entries); diagnostics. */
+int dbsp_schedule_download(const dbsp_schedule* sched, void* items_out, uint32_t* entries_out,
+                           uint64_t max_entries);
 /* Stats of the last build: items, entries (tile visits), dense tiles. */
 int dbsp_schedule_stats(const dbsp_schedule* sched, uint64_t* items, uint64_t* tile_visits,
                         uint64_t* dense_tiles);

@@ -62,6 +62,34 @@ class AttentionSchedule:
         check(L.lib().dbsp_schedule_build(self._h, C.byref(masks.c()), C.byref(view), int(pair_q)))
         return self
 
+    def build_device(self, words: torch.Tensor, num_kv_blocks: int, *, head_ids=None, q_block_ids=None,
+                     kv_block_ids=None, kv_tokens_global: int = 0, flags: int = 1,
+                     stream: Optional[torch.cuda.Stream] = None) -> "AttentionSchedule":
+        """K2: build the work list on the GPU from device mask words (int64
+        [H, Nq, ceil(Nk/64)], the BlockMask row layout)."""
+        if not words.is_cuda or words.dtype != torch.int64 or words.dim() != 3 or not words.is_contiguous():
+            raise ContractError("device mask words must be a contiguous CUDA int64 [H, Nq, words] tensor")
+        H, nq, _ = words.shape
+        hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
+        self._keep = (hid, qid, kid, words)
+        ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32)) if a is not None else None
+        view = L.LocalViewT(len(hid) if hid is not None else H, ptr(hid),
+                            len(qid) if qid is not None else nq, ptr(qid),
+                            len(kid) if kid is not None else num_kv_blocks, ptr(kid), kv_tokens_global)
+        s = stream if stream is not None else torch.cuda.current_stream(words.device)
+        check(L.lib().dbsp_schedule_build_device(self._h, C.c_void_p(words.data_ptr()), H, nq, num_kv_blocks,
+                                                 C.byref(view), int(flags), C.c_void_p(s.cuda_stream)))
+        return self
+
+    def download(self):
+        """(items [n, 8] uint32, entries uint32) of the built list."""
+        st = self.stats()
+        items = np.zeros((st["items"], 8), np.uint32)
+        entries = np.zeros(max(st["tile_visits"], 1), np.uint32)
+        check(L.lib().dbsp_schedule_download(self._h, C.c_void_p(items.ctypes.data),
+                                             entries.ctypes.data_as(C.POINTER(C.c_uint32)), entries.size))
+        return items, entries[:st["tile_visits"]]
+
     def stats(self) -> dict:
         items, visits, dense = C.c_uint64(), C.c_uint64(), C.c_uint64()
         check(L.lib().dbsp_schedule_stats(self._h, C.byref(items), C.byref(visits), C.byref(dense)))
@@ -114,7 +142,8 @@ def accum_init(o_accum: torch.Tensor, lse_accum: torch.Tensor, stream=None) -> N
 
 def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, masks: AttentionMaskSet, *,
                      softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
-                     return_lse: bool = False, schedule: Optional[AttentionSchedule] = None):
+                     return_lse: bool = False, schedule: Optional[AttentionSchedule] = None,
+                     device_schedule: bool = False):
     """O = softmax(Q K^T * scale) V restricted to the dense 64x64 tiles of
     `masks` (bit (q, k) of head h set => tile computed; reference
     mask.hpp:18-20).  q: [Sq, H, d], k/v: [Sk, H, d], bf16 CUDA, d in {64, 128}.
@@ -130,7 +159,12 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, masks: A
         out = torch.empty_like(q)
     lse = torch.empty((H, Sq), dtype=torch.float32, device=q.device) if return_lse else None
     sched = schedule
-    if sched is None:
+    if sched is None and device_schedule:
+        # K2: masks go to the device (1.3 MB for the Wan layer) and the work
+        # list is built there; no host pass over the masks, no list upload.
+        words = torch.from_numpy(masks.words.view(np.int64)).to(q.device, non_blocking=True)
+        sched = AttentionSchedule().build_device(words, masks.num_kv_blocks, kv_tokens_global=Sk)
+    elif sched is None:
         sched = AttentionSchedule().build(masks, kv_tokens_global=Sk)
     sched.launch(q, k, v, out, lse=lse, softmax_scale=softmax_scale)
     if schedule is None:

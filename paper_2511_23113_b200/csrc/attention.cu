@@ -187,14 +187,31 @@ struct dbsp_schedule {
   size_t pinned_bytes = 0;
   cudaEvent_t uploaded = nullptr;
   bool pending = false;
+  // device-built schedule (K2): items/entries live only in `dev`
+  bool on_device = false;
+  uint32_t dev_items = 0;
+  void* view_dev = nullptr;  // head ids, q ids, present bitmap, kv_local table
+  size_t view_bytes = 0;
+  void* k2_scratch = nullptr;
+  size_t k2_scratch_bytes = 0;
 
   ~dbsp_schedule() {
     if (pending && uploaded) cudaEventSynchronize(uploaded);
     if (dev) cudaFree(dev);
     if (pinned) cudaFreeHost(pinned);
     if (uploaded) cudaEventDestroy(uploaded);
+    if (view_dev) cudaFree(view_dev);
+    if (k2_scratch) cudaFree(k2_scratch);
   }
 };
+
+namespace dbsp_k2 {
+void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global,
+           const dbsp_core::LocalView& v, uint32_t flags, const uint32_t* d_head_ids,
+           const uint32_t* d_q_ids, const uint64_t* d_present, const int32_t* d_kv_local,
+           dbsp_core::WorkItem* items_out, uint32_t* entries_out, void*& scratch,
+           size_t& scratch_bytes, cudaStream_t stream);
+}
 
 using dbsp_capi::guard;
 
@@ -272,6 +289,89 @@ int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
     }
     build_schedule(m, lv, uint32_t(flags), sched->host);
     sched->dirty = true;
+    sched->on_device = false;
+  });
+}
+
+int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, uint32_t heads,
+                               uint32_t q_blocks, uint32_t kv_blocks, const dbsp_local_view* view,
+                               int32_t flags, void* stream_ptr) {
+  return guard([&] {
+    if (!sched || !d_words) fail(kContract, "null schedule or mask words");
+    if (heads == 0 || q_blocks == 0 || kv_blocks == 0) fail(kConfig, "mask dimensions must be positive");
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
+    LocalView lv;
+    lv.heads = view ? view->num_heads : heads;
+    lv.q_blocks = view ? view->num_q_blocks : q_blocks;
+    lv.kv_blocks = view ? view->num_kv_blocks : kv_blocks;
+    lv.kv_tokens_global = view ? view->kv_tokens_global : 0;
+    if (lv.heads == 0 || lv.q_blocks == 0 || lv.kv_blocks == 0)
+      fail(kConfig, "local view dimensions must be positive");
+    const uint32_t wpr = (kv_blocks + 63) / 64;
+    // Host-side view tables (small), uploaded with the build.
+    std::vector<uint32_t> hid(lv.heads), qid(lv.q_blocks);
+    std::vector<uint64_t> present(wpr, 0);
+    std::vector<int32_t> kvl(kv_blocks, -1);
+    for (uint32_t i = 0; i < lv.heads; ++i) {
+      hid[i] = view && view->head_ids ? view->head_ids[i] : i;
+      if (hid[i] >= heads) fail(kContract, "local head maps past the mask set");
+    }
+    for (uint32_t i = 0; i < lv.q_blocks; ++i) {
+      qid[i] = view && view->q_block_ids ? view->q_block_ids[i] : i;
+      if (qid[i] >= q_blocks) fail(kContract, "local Q block maps past the mask grid");
+    }
+    for (uint32_t i = 0; i < lv.kv_blocks; ++i) {
+      const uint32_t k = view && view->kv_block_ids ? view->kv_block_ids[i] : i;
+      if (k >= kv_blocks) fail(kContract, "local KV block maps past the mask grid");
+      if (kvl[k] >= 0) fail(kContract, "KV block listed twice in the local view");
+      kvl[k] = int32_t(i);
+      present[k / 64] |= 1ull << (k % 64);
+    }
+    const size_t vb = hid.size() * 4 + qid.size() * 4 + present.size() * 8 + kvl.size() * 4 + 64;
+    if (sched->view_bytes < vb) {
+      if (sched->view_dev) cudaFree(sched->view_dev);
+      sched->view_dev = nullptr;
+      cuda_check(cudaMalloc(&sched->view_dev, vb), "cudaMalloc view");
+      sched->view_bytes = vb;
+    }
+    uint8_t* vd = static_cast<uint8_t*>(sched->view_dev);
+    uint64_t* d_present = reinterpret_cast<uint64_t*>(vd);  // 8-byte aligned first
+    uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + present.size() * 8);
+    uint32_t* d_qid = d_hid + hid.size();
+    int32_t* d_kvl = reinterpret_cast<int32_t*>(d_qid + qid.size());
+    cuda_check(cudaMemcpyAsync(d_present, present.data(), present.size() * 8, cudaMemcpyHostToDevice, stream), "view");
+    cuda_check(cudaMemcpyAsync(d_hid, hid.data(), hid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
+    cuda_check(cudaMemcpyAsync(d_qid, qid.data(), qid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
+    cuda_check(cudaMemcpyAsync(d_kvl, kvl.data(), kvl.size() * 4, cudaMemcpyHostToDevice, stream), "view");
+    const uint32_t step = (flags & kSchedPairQ) ? 2 : 1;
+    const uint32_t n = lv.heads * ((lv.q_blocks + step - 1) / step);
+    const size_t item_bytes = size_t(n) * sizeof(WorkItem);
+    const size_t bytes = item_bytes + size_t(n) * lv.kv_blocks * sizeof(uint32_t);
+    if (sched->pending) {
+      cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
+      sched->pending = false;
+    }
+    if (sched->dev_bytes < bytes) {
+      if (sched->dev) cudaFree(sched->dev);
+      sched->dev = nullptr;
+      cuda_check(cudaMalloc(&sched->dev, bytes), "cudaMalloc schedule");
+      sched->dev_bytes = bytes;
+    }
+    dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, uint32_t(flags), d_hid, d_qid, d_present, d_kvl,
+                   static_cast<WorkItem*>(sched->dev),
+                   reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(sched->dev) + item_bytes),
+                   sched->k2_scratch, sched->k2_scratch_bytes, stream);
+    // Bounds for the launch-time checks; the host copy of the list is empty.
+    sched->host.items.clear();
+    sched->host.entries.clear();
+    sched->host.tile_visits = sched->host.dense_tiles = 0;
+    sched->host.max_head = lv.heads - 1;
+    sched->host.max_q_block = lv.q_blocks - 1;
+    sched->host.max_kv_block = lv.kv_blocks - 1;
+    sched->on_device = true;
+    sched->dirty = false;
+    sched->dev_items = n;
+    sched->item_bytes = item_bytes;
   });
 }
 
@@ -279,9 +379,48 @@ int dbsp_schedule_stats(const dbsp_schedule* s, uint64_t* items, uint64_t* visit
                         uint64_t* dense) {
   return guard([&] {
     if (!s) fail(kContract, "null schedule");
-    if (items) *items = s->host.items.size();
-    if (visits) *visits = s->host.tile_visits;
-    if (dense) *dense = s->host.dense_tiles;
+    if (!s->on_device) {
+      if (items) *items = s->host.items.size();
+      if (visits) *visits = s->host.tile_visits;
+      if (dense) *dense = s->host.dense_tiles;
+      return;
+    }
+    // Device-built: read the list back (synchronous; diagnostics only).
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    std::vector<WorkItem> it(s->dev_items);
+    cuda_check(cudaMemcpy(it.data(), s->dev, it.size() * sizeof(WorkItem), cudaMemcpyDeviceToHost), "d2h");
+    uint64_t n = 0;
+    for (const WorkItem& w : it) n += w.count;
+    std::vector<uint32_t> e(n);
+    if (n)
+      cuda_check(cudaMemcpy(e.data(), static_cast<uint8_t*>(s->dev) + s->item_bytes, n * 4,
+                            cudaMemcpyDeviceToHost), "d2h");
+    uint64_t dn = 0;
+    for (uint32_t x : e) dn += ((x & kEntryDenseA) != 0) + ((x & kEntryDenseB) != 0);
+    if (items) *items = s->dev_items;
+    if (visits) *visits = n;
+    if (dense) *dense = dn;
+  });
+}
+
+int dbsp_schedule_download(const dbsp_schedule* s, void* items_out, uint32_t* entries_out,
+                           uint64_t max_entries) {
+  return guard([&] {
+    if (!s || !items_out) fail(kContract, "null argument");
+    if (!s->on_device) {
+      std::memcpy(items_out, s->host.items.data(), s->host.items.size() * sizeof(WorkItem));
+      if (s->host.entries.size() > max_entries) fail(kContract, "entries buffer too small");
+      if (entries_out) std::memcpy(entries_out, s->host.entries.data(), s->host.entries.size() * 4);
+      return;
+    }
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    cuda_check(cudaMemcpy(items_out, s->dev, size_t(s->dev_items) * sizeof(WorkItem), cudaMemcpyDeviceToHost), "d2h");
+    uint64_t n = 0;
+    for (uint32_t i = 0; i < s->dev_items; ++i) n += static_cast<const WorkItem*>(items_out)[i].count;
+    if (n > max_entries) fail(kContract, "entries buffer too small");
+    if (entries_out && n)
+      cuda_check(cudaMemcpy(entries_out, static_cast<uint8_t*>(s->dev) + s->item_bytes, n * 4,
+                            cudaMemcpyDeviceToHost), "d2h");
   });
 }
 
@@ -312,13 +451,14 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     if ((!acc || a->finalize) && !a->o) fail(kContract, "null output");
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     const Schedule& h = sched->host;
-    if (h.items.empty()) return;
+    const uint32_t n_items = sched->on_device ? sched->dev_items : uint32_t(h.items.size());
+    if (n_items == 0) return;
     const uint32_t q_blocks = (a->q_tokens + 63) / 64, kv_blocks = (a->kv_tokens + 63) / 64;
     if (h.max_head >= a->heads || h.max_q_block >= q_blocks)
       fail(kContract, "schedule addresses past the Q buffer");
-    if (!h.entries.empty() && h.max_kv_block >= kv_blocks)
+    if ((sched->on_device || !h.entries.empty()) && h.max_kv_block >= kv_blocks)
       fail(kContract, "schedule addresses past the K/V buffers");
-    upload_schedule(sched, stream);
+    if (!sched->on_device) upload_schedule(sched, stream);
 
     dbsp_dev::AttnParams prm;
     prm.items = static_cast<const WorkItem*>(sched->dev);
@@ -338,7 +478,6 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
-    const uint32_t n_items = uint32_t(h.items.size());
     if (a->head_dim == 128 && use_wide())
       launch_wide(tk, tv, prm, n_items, stream);
     else if (use_split() && a->head_dim == 128)
@@ -346,9 +485,9 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     else if (use_split())
       launch_split<64>(tq, tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128)
-      launch_kernel<128>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
+      launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
     else
-      launch_kernel<64>(tq, tk, tv, prm, uint32_t(h.items.size()), stream);
+      launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
   });
 }
 

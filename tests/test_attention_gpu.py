@@ -149,6 +149,41 @@ def test_partitioned_execution_matches_one_shot(strategy):
         assert float((out.float() - full.float()).abs().max()) < 1e-2
 
 
+@pytest.mark.parametrize("case", ["identity", "rank_view", "ragged"])
+def test_device_schedule_matches_host(case):
+    # K2 on the GPU builds exactly the host builder's list (items, order, entries).
+    from paper_2511_23113_b200.sp import rank_layouts
+    H, nb = 8, 96
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.1, 0.6, 1.0, 11))
+    words = torch.from_numpy(masks.words.view(np.int64)).cuda()
+    kw = {}
+    S = nb * 64
+    if case == "rank_view":
+        st = D.ParallelStrategy(2, 4)
+        lay = rank_layouts(st, D.plan_dual(masks, st).plan, nb, nb)[5]
+        kw = dict(head_ids=lay.heads, q_block_ids=lay.q_blocks, kv_block_ids=lay.kv_groups[2])
+    if case == "ragged":
+        S = nb * 64 - 37
+    host = AttentionSchedule().build(masks, kv_tokens_global=S, **kw)
+    dev = AttentionSchedule().build_device(words, nb, kv_tokens_global=S, **kw)
+    hi, he = host.download()
+    di, de = dev.download()
+    assert np.array_equal(hi, di)
+    assert np.array_equal(he, de)
+    assert host.stats() == dev.stats()
+
+
+def test_device_schedule_attention_equal():
+    H, S, d = 8, 4096, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 2))
+    q, k, v = (t.cuda() for t in make_qkv(S, H, d, 3))
+    a = sparse_attention(q, k, v, masks)
+    b = sparse_attention(q, k, v, masks, device_schedule=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
 def test_nccl_executor_single_rank():
     # The NCCL-backed executor (the N>1 bench leg) on a 1-rank group: device
     # index tensors, buffers and the K4 launch path through SPAttention.
