@@ -360,6 +360,12 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* args, void
 /* Convenience: build + launch for a whole single-GPU problem (identity view). */
 int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, void* stream);
 
+/* Strided host<->device copy (cudaMemcpy2DAsync): moves a head slice of a
+ * token-major [tokens, heads, d] tensor, so host-resident layers can stream
+ * to the GPU in head chunks that overlap with K4 (see e2e.py). */
+int dbsp_copy_2d(void* dst, uint64_t dst_pitch, const void* src, uint64_t src_pitch,
+                 uint64_t width, uint64_t rows, int32_t to_device, void* stream);
+
 /* Accumulator init for a ring: o_accum = 0, lse_accum = -inf. */
 int dbsp_accum_init(float* o_accum, float* lse_accum, uint32_t q_tokens, uint32_t heads,
                     uint32_t head_dim, void* stream);

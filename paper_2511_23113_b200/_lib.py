@@ -155,6 +155,7 @@ _SIGS = {
     "dbsp_attention_launch": (C.c_int, [C.c_void_p, P(AttnArgsT), C.c_void_p]),
     "dbsp_sparse_attention": (C.c_int, [P(MaskSetT), P(AttnArgsT), C.c_void_p]),
     "dbsp_accum_init": (C.c_int, [C.c_void_p, C.c_void_p, u32, u32, u32, C.c_void_p]),
+    "dbsp_copy_2d": (C.c_int, [C.c_void_p, u64, C.c_void_p, u64, u64, u64, i32, C.c_void_p]),
     "dbsp_mask_stats_device": (C.c_int, [C.c_void_p, u32, u32, u32, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]),
 }

@@ -517,6 +517,17 @@ int dbsp_debug_set_trace(unsigned long long* dev) {
   return 0;
 }
 
+int dbsp_copy_2d(void* dst, uint64_t dst_pitch, const void* src, uint64_t src_pitch,
+                 uint64_t width, uint64_t rows, int32_t to_device, void* stream) {
+  return guard([&] {
+    if (!dst || !src) fail(kContract, "null pointer");
+    cuda_check(cudaMemcpy2DAsync(dst, dst_pitch, src, src_pitch, width, rows,
+                                 to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                                 reinterpret_cast<cudaStream_t>(stream)),
+               "cudaMemcpy2DAsync");
+  });
+}
+
 int dbsp_accum_init(float* o_accum, float* lse_accum, uint32_t q_tokens, uint32_t heads,
                     uint32_t head_dim, void* stream) {
   return guard([&] {

@@ -184,6 +184,22 @@ def test_device_schedule_attention_equal():
     assert torch.equal(a, b)
 
 
+def test_host_streaming_equals_one_shot():
+    # Head-chunked H2D / K4 / D2H overlap returns exactly the one-shot result.
+    from paper_2511_23113_b200.e2e import HostStreamingAttention
+    H, S, d = 10, 2048, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 4))
+    q, k, v = make_qkv(S, H, d, 8)
+    ref = sparse_attention(q.cuda(), k.cuda(), v.cuda(), masks).cpu()
+    run = HostStreamingAttention(S, H, d, chunks=3)
+    qh, kh, vh = (t.pin_memory() for t in (q, k, v))
+    for _ in range(2):
+        out = run(qh, kh, vh, masks)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+
+
 def test_nccl_executor_single_rank():
     # The NCCL-backed executor (the N>1 bench leg) on a 1-rank group: device
     # index tensors, buffers and the K4 launch path through SPAttention.
