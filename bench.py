@@ -145,12 +145,19 @@ def cpu_attention_baseline(wl, masks, budget_s: float = 8.0, seed: int = 7) -> d
             "sampled_seconds": elapsed}
 
 
+def wl_key(wl) -> str:
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    return next((k for k, v in WORKLOADS.items() if v is wl), "")
+
+
 def reference_planner_baseline(wl, gpus: int = 8, reps: int = 2) -> dict | None:
     """The reference's own planner (compiled from its headers into
     oracle/_ref/ref_bench; single thread as in the reference) on this
     workload's masks: select() and plan_dual per strategy."""
     tool = ROOT / "oracle" / "_ref" / "ref_bench"
-    prof = ROOT / "paper_2511_23113_b200" / "profiles" / "b200_nominal.json"
+    prof = ROOT / "paper_2511_23113_b200" / "profiles" / f"b200_{wl_key(wl)}_measured.json"
+    if not prof.exists():
+        prof = ROOT / "paper_2511_23113_b200" / "profiles" / "b200_nominal.json"
     if not tool.exists() or not prof.exists():
         return None
     out = subprocess.run([str(tool), str(wl.heads), str(wl.blocks), str(wl.blocks), wl.pattern,
@@ -250,7 +257,7 @@ def run_single(args, wl):
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
-    res["planner"] = planner_timing(masks)
+    res["planner"] = planner_timing(masks, workload=args.workload)
     if args.sp_sim > 1:
         res["sp_projection"] = sp_projection(q, k, v, masks, args.sp_sim)
     if not args.no_cpu_baseline:
@@ -264,19 +271,21 @@ def run_single(args, wl):
     return res
 
 
-def planner_timing(masks, G: int = 8, reps: int = 5) -> dict:
+def planner_timing(masks, G: int = 8, reps: int = 5, workload: str = None) -> dict:
     """Our host planner on the bench masks: select() over the G-GPU strategies
     (fresh SelectorState per call, as ref_bench times the reference)."""
     import paper_2511_23113_b200 as D
-    from paper_2511_23113_b200.sp_bench import load_profile
-    prof = load_profile()
+    from paper_2511_23113_b200.sp_bench import PROFILE, load_profile
+    prof = load_profile(workload)
+    measured = PROFILE.parent / f"b200_{workload}_measured.json"
     D.select(0, masks, prof, D.PlannerConfig(), D.SelectorState(G))
     t0 = time.perf_counter()
     for i in range(reps):
         sel = D.select(i, masks, prof, D.PlannerConfig(), D.SelectorState(G))
     ms = (time.perf_counter() - t0) / reps * 1e3
     return {"select_ms_per_call": round(ms, 3), "gpus_planned": G, "selected": str(sel.strategy),
-            "rho_s_post": round(sel.outcome.rho_post, 4), "profile": "b200_nominal.json",
+            "rho_s_post": round(sel.outcome.rho_post, 4),
+            "profile": measured.name if workload and measured.exists() else "b200_nominal.json",
             "threads": os.cpu_count()}
 
 

@@ -21,15 +21,21 @@ ROOT = Path(__file__).resolve().parents[1]
 PROFILE = Path(__file__).resolve().parent / "profiles" / "b200_nominal.json"
 
 
-def load_profile() -> P.MachineProfile:
+def load_profile(workload: str = None) -> P.MachineProfile:
+    """B200 MachineProfile for the selector: the measured one for this
+    workload shape (tests/measure_profile.py) when present, else nominal."""
+    if workload:
+        measured = PROFILE.parent / f"b200_{workload}_measured.json"
+        if measured.exists():
+            return P.MachineProfile.from_json(json.loads(measured.read_text()))
     return P.MachineProfile.from_json(json.loads(PROFILE.read_text()))
 
 
-def choose(masks, world: int, strategy: str, balance: str):
+def choose(masks, world: int, strategy: str, balance: str, workload: str = None):
     """Strategy + plan for this call: `auto` runs the U x R selector
     (selector.hpp:55-75) on the live masks; otherwise the named split."""
     if strategy == "auto":
-        sel = P.select(0, masks, load_profile(), P.PlannerConfig(), P.SelectorState(world))
+        sel = P.select(0, masks, load_profile(workload), P.PlannerConfig(), P.SelectorState(world))
         st = sel.strategy
     else:
         st = P.parse_strategy(strategy)
@@ -47,7 +53,7 @@ def run_distributed(args, wl, rank: int, world: int):
     dist.init_process_group("nccl", device_id=dev)
     try:
         masks = P.generate_mask_set(wl.spec())
-        st, plan = choose(masks, world, args.strategy, args.balance)
+        st, plan = choose(masks, world, args.strategy, args.balance, args.workload)
         H, S, d, nb = wl.heads, wl.tokens, wl.head_dim, wl.blocks
         g = torch.Generator(device=dev).manual_seed(1234)
         q = torch.randn(S, H, d, device=dev, dtype=torch.bfloat16, generator=g)
