@@ -313,7 +313,8 @@ void dbsp_schedule_destroy(dbsp_schedule* sched);
  * M=128 path).  Launch order is heaviest-first; GLOBAL_LPT orders across
  * heads, HEAD_ORDER within each head (K/V of concurrently running CTAs stays
  * L2-resident); with neither, small local problems get GLOBAL_LPT. */
-enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4 };
+enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4,
+       DBSP_SCHED_QUAD = 8 /* 4 Q blocks per item, for the 2-CTA (cta_group::2) K4 */ };
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
                         const dbsp_local_view* view, int32_t flags);

@@ -50,8 +50,13 @@ class AttentionSchedule:
 
     def build(self, masks: AttentionMaskSet, *, head_ids: Sequence[int] = None,
               q_block_ids: Sequence[int] = None, kv_block_ids: Sequence[int] = None,
-              kv_tokens_global: int = 0, pair_q: bool = True) -> "AttentionSchedule":
+              kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None
+              ) -> "AttentionSchedule":
+        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 8 quad =
+        the d=128 CTA-pair kernel); default pair_q."""
         hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
+        if flags is None:
+            flags = 1 if pair_q else 0
         self._keep = (hid, qid, kid)
         ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32)) if a is not None else None
         view = L.LocalViewT(
@@ -59,7 +64,7 @@ class AttentionSchedule:
             len(qid) if qid is not None else masks.num_q_blocks, ptr(qid),
             len(kid) if kid is not None else masks.num_kv_blocks, ptr(kid),
             kv_tokens_global)
-        check(L.lib().dbsp_schedule_build(self._h, C.byref(masks.c()), C.byref(view), int(pair_q)))
+        check(L.lib().dbsp_schedule_build(self._h, C.byref(masks.c()), C.byref(view), int(flags)))
         return self
 
     def build_device(self, words: torch.Tensor, num_kv_blocks: int, *, head_ids=None, q_block_ids=None,

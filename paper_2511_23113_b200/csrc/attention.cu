@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "attn_kernel.cuh"
+#include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
@@ -90,11 +91,12 @@ EncodeTiledFn encode_fn() {
 
 // [tokens, heads, d] bf16, box = 64 tokens x 1 head x 64 columns, 128B swizzle
 // (the layout the UMMA SW128 descriptors of attn_kernel.cuh expect).
-CUtensorMap make_tmap(const void* ptr, uint32_t tokens, uint32_t heads, uint32_t d) {
+CUtensorMap make_tmap(const void* ptr, uint32_t tokens, uint32_t heads, uint32_t d,
+                      uint32_t box_rows = 64) {
   CUtensorMap m;
   const cuuint64_t dims[3] = {d, heads, tokens};
   const cuuint64_t strides[2] = {cuuint64_t(d) * 2, cuuint64_t(heads) * d * 2};
-  const cuuint32_t box[3] = {64, 1, 64};
+  const cuuint32_t box[3] = {64, 1, box_rows};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -159,6 +161,21 @@ bool use_split() {
     return e && e[0] == '1';
   }();
   return split;
+}
+
+void launch_pair(const CUtensorMap& q, const CUtensorMap& k32, const CUtensorMap& v,
+                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::PairCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pair_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pair)");
+  dbsp_dev::sparse_attn_fwd_pair_kernel<<<2 * items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(
+      q, k32, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pair launch");
 }
 
 // d=128 kernel choice.  The 128-key-step variant (one CTA/SM) measured 6.96 ms
@@ -478,7 +495,11 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
-    if (a->head_dim == 128 && use_wide())
+    const bool quad = !sched->on_device && (h.flags & kSchedQuad);
+    if (quad && a->head_dim != 128) fail(kConfig, "quad (CTA-pair) schedules need head_dim 128");
+    if (quad)
+      launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
+    else if (a->head_dim == 128 && use_wide())
       launch_wide(tk, tv, prm, n_items, stream);
     else if (use_split() && a->head_dim == 128)
       launch_split<128>(tq, tk, tv, prm, n_items, stream);

@@ -49,9 +49,48 @@ void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Sched
   raw.reserve(size_t(v.heads) * ((v.q_blocks + 1) / 2));
   out.tile_visits = 0;
   out.dense_tiles = 0;
-  const uint32_t step = pair_q ? 2 : 1;
+  const bool quad = (flags & kSchedQuad) != 0;
+  const uint32_t step = quad ? 4 : pair_q ? 2 : 1;
   std::vector<uint64_t> uni(wpr);
-  for (uint32_t hl = 0; hl < v.heads; ++hl) {
+  for (uint32_t hl = 0; hl < v.heads && quad; ++hl) {
+    // Four Q blocks per item (two 128-row tiles of a CTA pair), one KV list:
+    // the union of the four rows; entry bit 22+i marks row i dense.
+    const uint32_t h = gh(hl);
+    for (uint32_t a = 0; a < v.q_blocks; a += 4) {
+      uint32_t q[4];
+      const uint64_t* rows[4];
+      uint32_t pad = 0;
+      for (uint32_t i = 0; i < 4; ++i) {
+        const bool in = a + i < v.q_blocks;
+        q[i] = in ? a + i : a;
+        rows[i] = in ? m.row(h, gq(q[i])) : nullptr;
+        pad |= in ? 0u : (1u << i);
+      }
+      Raw r;
+      r.it = WorkItem{hl, q[0], q[1], 0, 0, pad, q[2], q[3]};
+      for (size_t w = 0; w < wpr; ++w) {
+        uint64_t x = 0;
+        for (int i = 0; i < 4; ++i) x |= rows[i] ? rows[i][w] : 0ull;
+        uni[w] = x & present[w];
+      }
+      for (size_t w = 0; w < wpr; ++w)
+        for (uint64_t word = uni[w]; word; word &= word - 1) {
+          const uint32_t k = uint32_t(w * 64 + std::countr_zero(word));
+          const uint64_t bit = 1ull << (k % 64);
+          uint32_t e = local_of[k] | ((valid_keys(k) - 1) << kQuadValidShift);
+          for (uint32_t i = 0; i < 4; ++i)
+            if (rows[i] && (rows[i][w] & bit)) {
+              e |= 1u << (22 + i);
+              ++out.dense_tiles;
+            }
+          r.e.push_back(e);
+        }
+      r.it.count = uint32_t(r.e.size());
+      out.tile_visits += r.it.count;
+      raw.push_back(std::move(r));
+    }
+  }
+  for (uint32_t hl = 0; hl < v.heads && !quad; ++hl) {
     const uint32_t h = gh(hl);
     for (uint32_t a = 0; a < v.q_blocks; a += step) {
       const bool single = !pair_q || a + 1 >= v.q_blocks;
@@ -89,6 +128,7 @@ void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Sched
   });
   out.items.clear();
   out.entries.clear();
+  out.flags = flags;
   out.max_head = v.heads - 1;
   out.max_q_block = v.q_blocks - 1;
   out.max_kv_block = v.kv_blocks - 1;

@@ -10,7 +10,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 
 CHILD = r"""
-import sys, json, numpy as np, torch
+import os, sys, json, numpy as np, torch
 sys.path.insert(0, %r)
 import oracle, paper_2511_23113_b200 as D
 from paper_2511_23113_b200.attention import AttentionSchedule, sparse_attention
@@ -29,7 +29,8 @@ for name, (H, S, d, pat, lo, hi) in {"wan": (40, 32768, 128, "clustered", .15, .
     nb = S // 64
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pat, lo, hi, 1.0, 1))
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    sc = AttentionSchedule().build(m, kv_tokens_global=S); sc.upload()
+    fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1")) if d == 128 else 1
+    sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=fl); sc.upload()
     out = torch.empty_like(q)
     for _ in range(3): sc.launch(q, k, v, out)
     torch.cuda.synchronize()

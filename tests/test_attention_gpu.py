@@ -200,6 +200,28 @@ def test_host_streaming_equals_one_shot():
         assert torch.equal(out, ref)
 
 
+@pytest.mark.parametrize("H,S,Sk,pattern", [(4, 2048, None, "clustered"), (3, 1000, 2000, "random"),
+                                             (5, 4096, None, "banded")])
+def test_cta_pair_kernel(H, S, Sk, pattern):
+    # d=128 quad schedule -> the cta_group::2 kernel; odd block counts exercise
+    # padded rows of the quad.
+    Sk = Sk or S
+    d = 128
+    nq, nk = -(-S // 64), -(-Sk // 64)
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, pattern, 0.15, 0.6, 1.0, 17))
+    q, k, v = make_qkv(S, H, d, 19, Sk)
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                           masks.words, nk)
+    sc = AttentionSchedule().build(masks, kv_tokens_global=Sk, flags=1 | 8)
+    out = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
+    sc.launch(q.cuda(), k.cuda(), v.cuda(), out, lse=lse)
+    torch.cuda.synchronize()
+    check(out, ref, f"pair H{H} S{S} Sk{Sk} {pattern}")
+    fin = np.isfinite(ref_lse)
+    assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+
+
 def test_nccl_executor_single_rank():
     # The NCCL-backed executor (the N>1 bench leg) on a 1-rank group: device
     # index tensors, buffers and the K4 launch path through SPAttention.
