@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "attn_kernel.cuh"
+#include "attn_kernel_duo.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
@@ -176,6 +177,32 @@ void launch_pair(const CUtensorMap& q, const CUtensorMap& k32, const CUtensorMap
   dbsp_dev::sparse_attn_fwd_pair_kernel<<<2 * items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(
       q, k32, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_pair launch");
+}
+
+template <int D>
+void launch_duo(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::DuoCfg<D>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo_kernel<D>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(duo)");
+  dbsp_dev::sparse_attn_fwd_duo_kernel<D><<<items, dbsp_dev::kThreadsDuo, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo launch");
+}
+
+// Quad schedules run the two-stage kernel; DBSP_K4_PAIR=1 selects the
+// CTA-pair kernel instead (d=128 only; measured 8.19 ms vs 6.34 ms for the
+// pair-item kernel on the Wan layer).
+bool use_pair() {
+  static const bool pair = [] {
+    const char* e = std::getenv("DBSP_K4_PAIR");
+    return e && e[0] == '1';
+  }();
+  return pair;
 }
 
 // d=128 kernel choice.  The 128-key-step variant (one CTA/SM) measured 6.96 ms
@@ -496,9 +523,13 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
     const bool quad = !sched->on_device && (h.flags & kSchedQuad);
-    if (quad && a->head_dim != 128) fail(kConfig, "quad (CTA-pair) schedules need head_dim 128");
-    if (quad)
+    if (quad && use_pair() && a->head_dim != 128) fail(kConfig, "the CTA-pair kernel needs head_dim 128");
+    if (quad && use_pair())
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
+    else if (quad && a->head_dim == 128)
+      launch_duo<128>(tq, tk, tv, prm, n_items, stream);
+    else if (quad)
+      launch_duo<64>(tq, tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128 && use_wide())
       launch_wide(tk, tv, prm, n_items, stream);
     else if (use_split() && a->head_dim == 128)

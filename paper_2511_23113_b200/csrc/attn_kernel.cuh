@@ -133,6 +133,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const WorkItem it = p.items[blockIdx.x];
   const uint32_t count = it.count;
 
+#ifdef DBSP_TRACE_CTA
+  const unsigned long long c_start = clock64();
+  if (threadIdx.x == 0 && p.trace) p.trace[4 * blockIdx.x] = globaltimer_ns();
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(bKfull(s), 1);
@@ -361,24 +365,23 @@ __global__ void __launch_bounds__(kThreads, 2)
             tmem_st32(tmem + lane_off + C::kColO + c * 32, o);
           }
         }
-        const float negm = -m;
-        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+        // Packed f32x2 FMA/add (FFMA2/FADD2): half the non-MUFU issue slots.
+        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float x0 = fmaf(v[2 * i], sl2, negm);
-          const float x1 = fmaf(v[2 * i + 1], sl2, negm);
-          float p0, p1;
+          const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
+          float2 pp;
           if ((i % kPolyEvery) == kPolyEvery - 1) {  // FA4-style MUFU offload (off by default)
-            p0 = exp2_poly3(x0);
-            p1 = exp2_poly3(x1);
+            pp = make_float2(exp2_poly3(x.x), exp2_poly3(x.y));
           } else {
-            p0 = fast_exp2(x0);
-            p1 = fast_exp2(x1);
+            pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
           }
-          sum4[i & 3] += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
+          acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
+          pk[i] = pack_bf16x2(pp.x, pp.y);
         }
-        l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+        const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
+        l += a2.x + a2.y;
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) pk[i] = 0u;
@@ -477,6 +480,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem, kTmemCols);
+#ifdef DBSP_TRACE_CTA
+  if (threadIdx.x == 0 && p.trace) {
+    p.trace[4 * blockIdx.x + 1] = globaltimer_ns();
+    p.trace[4 * blockIdx.x + 2] = smid();
+    p.trace[4 * blockIdx.x + 3] = clock64() - c_start;
+  }
+#endif
 }
 
 }  // namespace dbsp_dev

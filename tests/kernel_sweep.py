@@ -29,7 +29,7 @@ for name, (H, S, d, pat, lo, hi) in {"wan": (40, 32768, 128, "clustered", .15, .
     nb = S // 64
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pat, lo, hi, 1.0, 1))
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1")) if d == 128 else 1
+    fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1"))
     sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=fl); sc.upload()
     out = torch.empty_like(q)
     for _ in range(3): sc.launch(q, k, v, out)
@@ -46,6 +46,10 @@ print("RESULT", json.dumps(res))
 
 
 def main():
+    if sys.argv[1:] == ["--no-build"]:  # time the in-tree build as is
+        out = subprocess.run([sys.executable, "-c", CHILD], capture_output=True, text=True, timeout=600)
+        print(out.stdout.strip() or out.stderr[-800:], flush=True)
+        return
     variants = sys.argv[1:] or [""]
     for flags in variants:
         env = dict(os.environ, DBSP_NVCC_FLAGS=flags)

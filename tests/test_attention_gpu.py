@@ -200,13 +200,14 @@ def test_host_streaming_equals_one_shot():
         assert torch.equal(out, ref)
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("H,S,Sk,pattern", [(4, 2048, None, "clustered"), (3, 1000, 2000, "random"),
-                                             (5, 4096, None, "banded")])
-def test_cta_pair_kernel(H, S, Sk, pattern):
-    # d=128 quad schedule -> the cta_group::2 kernel; odd block counts exercise
-    # padded rows of the quad.
+                                             (5, 4096, None, "banded"), (2, 448, 4000, "random")])
+def test_two_stage_kernel(H, S, Sk, pattern, d):
+    # quad schedule -> the two-stage kernel (two 128-row Q tiles per CTA,
+    # 128-key steps); odd block counts exercise padded rows of the quad and the
+    # masked second half of an odd-length step.
     Sk = Sk or S
-    d = 128
     nq, nk = -(-S // 64), -(-Sk // 64)
     masks = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, pattern, 0.15, 0.6, 1.0, 17))
     q, k, v = make_qkv(S, H, d, 19, Sk)
@@ -217,9 +218,33 @@ def test_cta_pair_kernel(H, S, Sk, pattern):
     lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
     sc.launch(q.cuda(), k.cuda(), v.cuda(), out, lse=lse)
     torch.cuda.synchronize()
-    check(out, ref, f"pair H{H} S{S} Sk{Sk} {pattern}")
+    check(out, ref, f"two-stage d{d} H{H} S{S} Sk{Sk} {pattern}")
     fin = np.isfinite(ref_lse)
     assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+    assert np.all(np.isneginf(lse.cpu().numpy()[~fin]))
+
+
+def test_two_stage_ring_accumulate():
+    # Two KV periods through accumulate + finalize on the two-stage kernel
+    # equal one pass over all KV (the K5 merge in its epilogue).
+    H, S, d = 3, 1536, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.2, 0.5, 1.0, 5))
+    q, k, v = make_qkv(S, H, d, 7)
+    ref, _ = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(), masks.words, nb)
+    qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
+    o_acc = torch.empty(S, H, d, device="cuda", dtype=torch.float32)
+    l_acc = torch.empty(H, S, device="cuda", dtype=torch.float32)
+    accum_init(o_acc, l_acc)
+    out = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
+    half = nb // 2
+    for p, ids in enumerate((list(range(half)), list(range(half, nb)))):
+        sc = AttentionSchedule().build(masks, kv_block_ids=ids, kv_tokens_global=S, flags=1 | 8)
+        sl = slice(ids[0] * 64, (ids[-1] + 1) * 64)
+        sc.launch(qc, kc[sl].contiguous(), vc[sl].contiguous(), out, o_accum=o_acc, lse_accum=l_acc,
+                  accumulate=True, finalize=p == 1)
+    torch.cuda.synchronize()
+    check(out, ref, "two-stage ring accumulate")
 
 
 def test_nccl_executor_single_rank():

@@ -15,7 +15,15 @@ sys.path.insert(0, str(ROOT))
 
 
 def main():
-    flags = "-DDBSP_TRACE " + " ".join(sys.argv[1:])
+    args = sys.argv[1:]
+    sched_flags = 1
+    if args[:1] == ["--sched"]:
+        sched_flags = int(args[1])
+        args = args[2:]
+    fine = args[:1] == ["--fine"]
+    if fine:
+        args = args[1:] + ["-DDBSP_TRACE_FINE"]
+    flags = "-DDBSP_TRACE " + " ".join(args)
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    env=dict(os.environ, DBSP_NVCC_FLAGS=flags), capture_output=True)
     import torch
@@ -30,13 +38,23 @@ def main():
     H, S, d = 40, 32768, 128
     m = D.generate_mask_set(D.GeneratorSpec(H, S // 64, S // 64, 64, "clustered", 0.15, 0.45, 1.0, 1))
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    sc = AttentionSchedule().build(m, kv_tokens_global=S)
+    sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=sched_flags)
     out = torch.empty_like(q)
     for _ in range(3):
         sc.launch(q, k, v, out)
     torch.cuda.synchronize()
     tr = buf.view(B, T, E).cpu().numpy().astype(np.int64)
     fn(None)
+    if sched_flags & 8 and fine:
+        fine_report(tr)
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
+    if sched_flags & 8:
+        duo_report(tr)
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
     names = ["soft_start", "soft_end", "mma_S", "mma_PV", "soft_start_hi", "soft_end_hi", "load_K", "load_V"]
     stats = {}
     for b in range(B):
@@ -62,6 +80,48 @@ def main():
     print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    capture_output=True)
+
+
+def fine_report(tr):
+    """Stage-0 softmax phases (DBSP_TRACE_FINE): start, S loaded, max, P halves stored, arrive."""
+    stats = {}
+    for b in range(tr.shape[0]):
+        t = tr[b].astype(np.int64)
+        n = int((t[:, 0] > 0).sum())
+        if n < 8:
+            continue
+        t = t[2:n]
+        for key, arr in [("ld_S", t[:, 2] - t[:, 0]), ("max", t[:, 6] - t[:, 2]), ("exp_half0", t[:, 3] - t[:, 6]),
+                         ("exp_half1", t[:, 4] - t[:, 3]), ("st_wait_arrive", t[:, 1] - t[:, 4]),
+                         ("total", t[:, 1] - t[:, 0]), ("P_to_PV0", t[:, 7] - t[:, 1]),
+                         ("wait_next_S", t[1:, 0] - t[:-1, 1])]:
+            stats.setdefault(key, []).append(float(np.median(arr)))
+    print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
+
+
+def duo_report(tr):
+    """Two-stage kernel events per 128-key step t (attn_kernel_duo.cuh)."""
+    names = ["sm0_start", "sm0_end", "sm1_start", "sm1_end", "S0_issued", "PV0_start", "S1_issued", "PV1_start"]
+    stats = {}
+    for b in range(tr.shape[0]):
+        t = tr[b]
+        n = int((t[:, 0] > 0).sum())
+        if n < 8:
+            continue
+        t = t[:n].astype(np.int64)
+        for key, arr in [("softmax0", t[:, 1] - t[:, 0]), ("softmax1", t[:, 3] - t[:, 2]),
+                         ("sm0_wait_for_S", t[1:, 0] - t[:-1, 1]), ("sm1_wait_for_S", t[1:, 2] - t[:-1, 3]),
+                         ("P0_to_PV0", t[:, 5] - t[:, 1]), ("P1_to_PV1", t[:, 7] - t[:, 3]),
+                         ("S0_issue_to_sm0", t[:, 0] - t[:, 4]), ("S1_issue_to_sm1", t[:, 2] - t[:, 6]),
+                         ("step_period", np.diff(t[:, 0]))]:
+            arr = arr[2:] if len(arr) > 4 else arr
+            stats.setdefault(key, []).append(float(np.median(arr)))
+        if b < 2:
+            print(f"block {b}: steps={n}")
+            base = t[0, 0]
+            for j in range(min(n, 10)):
+                print("  t=%2d " % j + " ".join(f"{nm}={int(t[j, e] - base):7d}" for e, nm in enumerate(names)))
+    print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
 
 
 if __name__ == "__main__":
