@@ -169,6 +169,28 @@ def reference_planner_baseline(wl, gpus: int = 8, reps: int = 2) -> dict | None:
 
 
 # ----------------------------------------------------------------------------- our arm, N = 1
+def kernel_clock_mhz(launch) -> float | None:
+    """SM clock inside one K4 launch: CTA 0 stamps clock64 and %globaltimer at
+    start and end (dbsp_debug_set_clock_probe); nvidia-smi's sampled clock can
+    miss the power-capped in-kernel value."""
+    import ctypes
+    import torch
+    from paper_2511_23113_b200 import _lib
+    fn = getattr(_lib.lib(), "dbsp_debug_set_clock_probe", None)
+    if fn is None:
+        return None
+    fn.argtypes = [ctypes.c_void_p]
+    buf = torch.zeros(4, dtype=torch.int64, device="cuda")
+    fn(ctypes.c_void_p(buf.data_ptr()))
+    try:
+        launch()
+        torch.cuda.synchronize()
+    finally:
+        fn(None)
+    c0, t0, c1, t1 = (int(x) for x in buf.cpu().tolist())
+    return round((c1 - c0) / (t1 - t0) * 1e3, 1) if t1 > t0 else None
+
+
 def run_single(args, wl):
     import numpy as np
     import torch
@@ -206,6 +228,7 @@ def run_single(args, wl):
         torch.cuda.synchronize()
     per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     ms = ev[0].elapsed_time(ev[-1]) / args.steps
+    kernel_mhz = kernel_clock_mhz(lambda: sched.launch(q, k, v, out))
     flops = wl.flops_per_block() * total
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
@@ -255,7 +278,9 @@ def run_single(args, wl):
                         f"{args.e2e_chunks} head chunks (cudaMemcpy2DAsync), mask words H2D, K2 list build + K4 "
                         "per chunk on the GPU, D2H of o -- copies overlap the kernel on 3 streams"},
         "gpu_launches": args.steps,
-        "clocks": clk.summary(),
+        "clocks": {**clk.summary(), "sm_mhz_in_kernel": kernel_mhz,
+                   "note": "sm_mhz: nvidia-smi samples over the timed region; sm_mhz_in_kernel: "
+                           "clock64 / %globaltimer of CTA 0 inside one more K4 launch right after it"},
     }
     res["planner"] = planner_timing(masks, workload=args.workload)
     if args.sp_sim > 1:

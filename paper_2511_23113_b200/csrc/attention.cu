@@ -218,6 +218,7 @@ bool use_wide() {
 }
 
 unsigned long long* g_trace = nullptr;
+unsigned long long* g_clock_probe = nullptr;
 
 }  // namespace
 
@@ -519,6 +520,7 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(float(a->head_dim));
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.trace = g_trace;
+    prm.clock_probe = g_clock_probe;
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
@@ -566,6 +568,13 @@ int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, 
 // tiles x 8 events u64 clock64 stamps, used by DBSP_TRACE builds.
 int dbsp_debug_set_trace(unsigned long long* dev) {
   g_trace = dev;
+  return 0;
+}
+
+// Debug hook (not in the public header): 4 x u64 device buffer that CTA 0 of
+// the default kernel fills with {clock64, globaltimer} at start and end.
+int dbsp_debug_set_clock_probe(unsigned long long* dev) {
+  g_clock_probe = dev;
   return 0;
 }
 

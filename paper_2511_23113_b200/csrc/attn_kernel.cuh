@@ -49,7 +49,17 @@ struct AttnParams {
   uint32_t mode;
   float scale_log2;
   unsigned long long* trace;  // DBSP_TRACE builds only: clock64 per (block, tile, event)
+  // Optional: CTA 0 writes {clock64, globaltimer} at start and end, so the host
+  // can read the SM clock the kernel actually ran at (power capping).
+  unsigned long long* clock_probe;
 };
+
+__device__ __forceinline__ void clock_probe_mark(const AttnParams& p, int slot) {
+  if (p.clock_probe && blockIdx.x == 0 && threadIdx.x == 0) {
+    p.clock_probe[2 * slot] = clock64();
+    p.clock_probe[2 * slot + 1] = globaltimer_ns();
+  }
+}
 
 // Event slots of the optional per-tile trace (DBSP_TRACE).
 enum : int { kTrSoftStart = 0, kTrSoftEnd, kTrMmaS, kTrMmaPV, kTrSoftStartHi, kTrSoftEndHi,
@@ -70,10 +80,18 @@ constexpr int kTraceBlocks = 16, kTraceTiles = 256;
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain
-#ifndef DBSP_POLY_EVERY
-#define DBSP_POLY_EVERY 1000
+// exp2 pairs (of every 8) computed on the FMA pipe (exp2_poly3_pair) instead
+// of MUFU.  Measured (tests/kernel_sweep.py): d=64 is MUFU-bound and runs
+// 1.83 ms with 2 of 8 vs 1.94 ms with none on the CogVideoX layer; d=128 is
+// smem-port bound and only slows down (6.47 vs 6.22 ms on Wan).
+template <int D>
+__host__ __device__ constexpr int poly_pairs() {
+#ifdef DBSP_POLY_N
+  return DBSP_POLY_N;
+#else
+  return D == 64 ? 2 : 0;
 #endif
-constexpr int kPolyEvery = DBSP_POLY_EVERY;  // 1 in kPolyEvery exp2 pairs on the FMA pipe
+}
 
 template <int D>
 struct KCfg {
@@ -133,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const WorkItem it = p.items[blockIdx.x];
   const uint32_t count = it.count;
 
+  clock_probe_mark(p, 0);
 #ifdef DBSP_TRACE_CTA
   const unsigned long long c_start = clock64();
   if (threadIdx.x == 0 && p.trace) p.trace[4 * blockIdx.x] = globaltimer_ns();
@@ -372,8 +391,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int i = 0; i < 32; ++i) {
           const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
           float2 pp;
-          if ((i % kPolyEvery) == kPolyEvery - 1) {  // FA4-style MUFU offload (off by default)
-            pp = make_float2(exp2_poly3(x.x), exp2_poly3(x.y));
+          if ((i & 7) < poly_pairs<D>()) {  // FA4-style MUFU offload
+            pp = exp2_poly3_pair(x);
           } else {
             pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
           }
@@ -480,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   if (warp == 5) tmem_dealloc(tmem, kTmemCols);
+  clock_probe_mark(p, 1);
 #ifdef DBSP_TRACE_CTA
   if (threadIdx.x == 0 && p.trace) {
     p.trace[4 * blockIdx.x + 1] = globaltimer_ns();

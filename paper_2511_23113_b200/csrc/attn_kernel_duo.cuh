@@ -342,8 +342,8 @@ __global__ void __launch_bounds__(kThreadsDuo, 1)
             for (int i = 0; i < 32; ++i) {
               const float2 x = __ffma2_rn(make_float2(v[64 * h + 2 * i], v[64 * h + 2 * i + 1]), sc2, nm2);
               float2 pp;
-              if ((i % kPolyEvery) == kPolyEvery - 1) {
-                pp = make_float2(exp2_poly3(x.x), exp2_poly3(x.y));
+              if ((i & 7) < poly_pairs<D>()) {
+                pp = exp2_poly3_pair(x);
               } else {
                 pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
               }

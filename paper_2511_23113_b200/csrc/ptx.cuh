@@ -287,6 +287,21 @@ __device__ __forceinline__ float exp2_poly3(float x) {
   return __int_as_float(__float_as_int(p) + (n << 23));
 }
 
+// Packed (f32x2) form of exp2_poly3 for a pair: FADD2/FFMA2 plus two shift-adds,
+// about 5 issue slots per result and no MUFU.
+__device__ __forceinline__ float2 exp2_poly3_pair(float2 x) {
+  x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 q = __ffma2_rn(f, make_float2(0.05500764772295952f, 0.05500764772295952f),
+                        make_float2(0.24220800399780273f, 0.24220800399780273f));
+  q = __ffma2_rn(q, f, make_float2(0.6932827234268188f, 0.6932827234268188f));
+  q = __ffma2_rn(q, f, make_float2(1.f, 1.f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

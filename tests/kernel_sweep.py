@@ -15,21 +15,24 @@ sys.path.insert(0, %r)
 import oracle, paper_2511_23113_b200 as D
 from paper_2511_23113_b200.attention import AttentionSchedule, sparse_attention
 res = {}
-# parity (toy + d128 clustered)
+fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1"))
+# parity (toy + d128 clustered) with the swept schedule flags
 for (H, S, d, pat, lo, hi, seed) in [(8, 4096, 64, "random", .5, .5, 1), (4, 2048, 128, "clustered", .1, .6, 3)]:
     nb = S // 64
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pat, lo, hi, 1.0, seed))
     g = torch.Generator().manual_seed(seed)
     q, k, v = (torch.randn(S, H, d, generator=g).to(torch.bfloat16) for _ in range(3))
     ref, _ = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(), m.words, nb)
-    out = sparse_attention(q.cuda(), k.cuda(), v.cuda(), m).float().cpu().numpy()
+    sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=fl)
+    o = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
+    sc.launch(q.cuda(), k.cuda(), v.cuda(), o)
+    out = o.float().cpu().numpy()
     res[f"maxabs_d{d}"] = float(np.abs(out - ref).max())
 for name, (H, S, d, pat, lo, hi) in {"wan": (40, 32768, 128, "clustered", .15, .45),
                                      "cog": (48, 17792, 64, "clustered", .317, .317)}.items():
     nb = S // 64
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pat, lo, hi, 1.0, 1))
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1"))
     sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=fl); sc.upload()
     out = torch.empty_like(q)
     for _ in range(3): sc.launch(q, k, v, out)

@@ -16,6 +16,25 @@
 #define FADD2(x, y) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y))
 #define EX2LO(x) asm volatile("{.reg .f32 lo, hi; mov.b64 {lo, hi}, %0; ex2.approx.ftz.f32 lo, lo; ex2.approx.ftz.f32 hi, hi; mov.b64 %0, {lo, hi};}" : "+l"(x))
 
+// 2^x for a pair on the FMA/ALU pipes (packed f32x2): clamp, round-to-int by
+// the 1.5*2^23 trick, degree-3 polynomial of the fraction, exponent by shift+add.
+__device__ __forceinline__ unsigned long long exp2_pair_poly(unsigned long long x) {
+  float lo = __uint_as_float(uint32_t(x)), hi = __uint_as_float(uint32_t(x >> 32));
+  lo = fmaxf(lo, -127.f);
+  hi = fmaxf(hi, -127.f);
+  float2 xv = make_float2(lo, hi);
+  const float2 mg = make_float2(12582912.f, 12582912.f), nmg = make_float2(-12582912.f, -12582912.f);
+  const float2 t = __fadd2_rn(xv, mg);
+  const float2 f = __fadd2_rn(xv, __fmul2_rn(__fadd2_rn(t, nmg), make_float2(-1.f, -1.f)));
+  float2 p = __ffma2_rn(f, make_float2(0.05500764772295952f, 0.05500764772295952f),
+                        make_float2(0.24220800399780273f, 0.24220800399780273f));
+  p = __ffma2_rn(p, f, make_float2(0.6932827234268188f, 0.6932827234268188f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  const uint32_t rl = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t rh = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return (unsigned long long)rh << 32 | rl;
+}
+
 // MODE 8: packed softmax body per pair: FFMA2, 2x ex2, FADD2, cvt (one pair = 2 elements)
 // MODE: 0 ex2 | 1 cvt | 2 ex2+cvt (2:1) | 3 fma | 4 max3 | 5 prmt | 6 ex2+fma (1:1)
 //       7 ex2 + cvt + 2 fma (the softmax body per pair: 2 ex2, 1 cvt, 2 ffma, 2 fadd)
@@ -34,9 +53,10 @@ __global__ void k(uint32_t* out, int iters) {
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (MODE == 8) {
+      if (MODE == 8 || (MODE >= 10 && MODE <= 14)) {
         FFMA2(pa[i], sc, ng);
-        EX2LO(pa[i]);
+        if (MODE >= 10 && i < MODE - 10) pa[i] = exp2_pair_poly(pa[i]);
+        else EX2LO(pa[i]);
         FADD2(ps, pa[i]);
         CVT(r[i], __uint_as_float(uint32_t(pa[i])), __uint_as_float(uint32_t(pa[i] >> 32)));
       }
@@ -103,6 +123,17 @@ int main() {
   run<6>("ex2 x8 + ffma x8", 16);
   run<7>("softmax body: ffma,ex2,fadd x8 + cvt x4", 28);
   run<8>("packed body: ffma2,2 ex2,fadd2,cvt x8 (16 elems)", 40);
+  run<11>("packed body, 1 of 8 pairs poly", 40);
+  run<12>("packed body, 2 of 8 pairs poly", 40);
+  run<13>("packed body, 3 of 8 pairs poly", 40);
+  run<14>("packed body, 4 of 8 pairs poly", 40);
+  run<11>("packed body, 1 of 8 pairs poly", 40, 148, 128);
+  run<12>("packed body, 2 of 8 pairs poly", 40, 148, 128);
+  run<13>("packed body, 3 of 8 pairs poly", 40, 148, 128);
+  run<14>("packed body, 4 of 8 pairs poly", 40, 148, 128);
+  run<12>("packed body, 2 of 8 pairs poly", 40, 148, 256);
+  run<13>("packed body, 3 of 8 pairs poly", 40, 148, 256);
+  run<14>("packed body, 4 of 8 pairs poly", 40, 148, 256);
   // one and two warps per SMSP: the two-stage kernel's softmax occupancy
   run<0>("ex2", 8, 148, 128);
   run<7>("softmax body: ffma,ex2,fadd x8 + cvt x4", 28, 148, 128);
