@@ -52,7 +52,7 @@ class AttentionSchedule:
               q_block_ids: Sequence[int] = None, kv_block_ids: Sequence[int] = None,
               kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None
               ) -> "AttentionSchedule":
-        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 8 quad =
+        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 16 with 8: 128-key steps, 8 quad =
         the d=128 CTA-pair kernel); default pair_q."""
         hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
         if flags is None:

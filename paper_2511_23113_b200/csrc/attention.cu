@@ -15,6 +15,7 @@
 
 #include "attn_kernel.cuh"
 #include "attn_kernel_duo.cuh"
+#include "attn_kernel_quad.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
@@ -194,7 +195,23 @@ void launch_duo(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo launch");
 }
 
-// Quad schedules run the two-stage kernel; DBSP_K4_PAIR=1 selects the
+template <int D>
+void launch_quad(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::QuadCfg<D>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_quad_kernel<D>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(quad)");
+  dbsp_dev::sparse_attn_fwd_quad_kernel<D><<<items, dbsp_dev::kThreadsQuad, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_quad launch");
+}
+
+// Quad schedules run the two-stage kernels (64-key steps, or 128-key steps
+// with DBSP_SCHED_KEY128); DBSP_K4_PAIR=1 selects the
 // CTA-pair kernel instead (d=128 only; measured 8.19 ms vs 6.34 ms for the
 // pair-item kernel on the Wan layer).
 bool use_pair() {
@@ -528,10 +545,14 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     if (quad && use_pair() && a->head_dim != 128) fail(kConfig, "the CTA-pair kernel needs head_dim 128");
     if (quad && use_pair())
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
-    else if (quad && a->head_dim == 128)
+    else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
       launch_duo<128>(tq, tk, tv, prm, n_items, stream);
-    else if (quad)
+    else if (quad && (h.flags & kSchedKey128))
       launch_duo<64>(tq, tk, tv, prm, n_items, stream);
+    else if (quad && a->head_dim == 128)
+      launch_quad<128>(tq, tk, tv, prm, n_items, stream);
+    else if (quad)
+      launch_quad<64>(tq, tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128 && use_wide())
       launch_wide(tk, tv, prm, n_items, stream);
     else if (use_split() && a->head_dim == 128)

@@ -395,79 +395,7 @@ __global__ void __launch_bounds__(kThreadsDuo, 1)
       mbar_wait(bOfinal(st), 0);
       tc_fence_after();
     }
-    const bool live = !padded && token < p.q_tokens;
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
-    const float kLn2 = 0.6931471805599453f;
-    const float lse_new = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
-    const size_t orow = (size_t(token) * p.heads + it.head) * D;
-    const size_t lidx = size_t(it.head) * p.q_tokens + token;
-
-    float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
-    const bool acc = (p.mode & kModeAccumulate) != 0;
-    if (acc) {
-      const float lse_old = live ? p.lse_acc[lidx] : -INFINITY;
-      const float mx = fmaxf(lse_old, lse_new);
-      if (mx == -INFINITY) {
-        c_old = 0.f;
-        c_new = 0.f;
-        lse_out = -INFINITY;
-      } else {
-        const float w_old = __expf(lse_old - mx);
-        const float w_new = __expf(lse_new - mx);
-        const float den = w_old + w_new;
-        c_old = w_old / den;
-        c_new = w_new * inv_l / den;
-        lse_out = mx + __logf(den);
-      }
-    }
-    const bool write_bf16 = !acc || (p.mode & kModeFinalize);
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      if (count > 0) {
-        tmem_ld32(ocol + c * 32, o);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0u;
-      }
-      if (!live) continue;
-      float r[32];
-      if (acc) {
-        float4* pa = reinterpret_cast<float4*>(p.o_acc + orow + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 a = pa[i];
-          a.x = a.x * c_old + __uint_as_float(o[4 * i + 0]) * c_new;
-          a.y = a.y * c_old + __uint_as_float(o[4 * i + 1]) * c_new;
-          a.z = a.z * c_old + __uint_as_float(o[4 * i + 2]) * c_new;
-          a.w = a.w * c_old + __uint_as_float(o[4 * i + 3]) * c_new;
-          pa[i] = a;
-          r[4 * i + 0] = a.x;
-          r[4 * i + 1] = a.y;
-          r[4 * i + 2] = a.z;
-          r[4 * i + 3] = a.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = __uint_as_float(o[i]) * inv_l;
-      }
-      if (write_bf16) {
-        uint4* po = reinterpret_cast<uint4*>(p.out + orow + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          po[i] = make_uint4(pack_bf16x2(r[8 * i + 0], r[8 * i + 1]),
-                             pack_bf16x2(r[8 * i + 2], r[8 * i + 3]),
-                             pack_bf16x2(r[8 * i + 4], r[8 * i + 5]),
-                             pack_bf16x2(r[8 * i + 6], r[8 * i + 7]));
-      }
-    }
-    if (live) {
-      if (acc)
-        p.lse_acc[lidx] = lse_out;
-      else if (p.lse)
-        p.lse[lidx] = lse_new;
-    }
+    finish_row<D>(p, ocol, count > 0, !padded && token < p.q_tokens, m, l, token, it.head);
   }
 
   tc_fence_before();

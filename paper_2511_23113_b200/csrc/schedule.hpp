@@ -47,14 +47,15 @@ struct Schedule {
   uint64_t tile_visits = 0;  // sum of counts (MMA tiles issued)
   uint64_t dense_tiles = 0;  // 64x64 tiles actually dense (softmax work)
   uint32_t max_head = 0, max_q_block = 0, max_kv_block = 0;  // bounds checked at launch
-  uint32_t flags = 0;  // build flags (kSchedQuad selects the CTA-pair kernel)
+  uint32_t flags = 0;  // build flags (kSchedQuad selects a two-stage kernel)
 };
 
 // Schedule flags (dbsp_schedule_build's `flags`).
 constexpr uint32_t kSchedPairQ = 1;      // two Q blocks per 128-row tile
 constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all heads
 constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
-constexpr uint32_t kSchedQuad = 8;       // four Q blocks per item (2-CTA kernel)
+constexpr uint32_t kSchedQuad = 8;       // four Q blocks per item (two-stage kernels)
+constexpr uint32_t kSchedKey128 = 16;    // with kSchedQuad: 128-key steps (attn_kernel_duo.cuh)
 // Quad items: WorkItem{head, q0, q1, begin, count, pad_mask, q2, q3}; entries
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
 constexpr uint32_t kQuadValidShift = 26;

@@ -200,10 +200,11 @@ def test_host_streaming_equals_one_shot():
         assert torch.equal(out, ref)
 
 
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("H,S,Sk,pattern", [(4, 2048, None, "clustered"), (3, 1000, 2000, "random"),
                                              (5, 4096, None, "banded"), (2, 448, 4000, "random")])
-def test_two_stage_kernel(H, S, Sk, pattern, d):
+def test_two_stage_kernel(H, S, Sk, pattern, d, flags):
     # quad schedule -> the two-stage kernel (two 128-row Q tiles per CTA,
     # 128-key steps); odd block counts exercise padded rows of the quad and the
     # masked second half of an odd-length step.
@@ -213,18 +214,19 @@ def test_two_stage_kernel(H, S, Sk, pattern, d):
     q, k, v = make_qkv(S, H, d, 19, Sk)
     ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
                                            masks.words, nk)
-    sc = AttentionSchedule().build(masks, kv_tokens_global=Sk, flags=1 | 8)
+    sc = AttentionSchedule().build(masks, kv_tokens_global=Sk, flags=flags)
     out = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
     sc.launch(q.cuda(), k.cuda(), v.cuda(), out, lse=lse)
     torch.cuda.synchronize()
-    check(out, ref, f"two-stage d{d} H{H} S{S} Sk{Sk} {pattern}")
+    check(out, ref, f"two-stage flags{flags} d{d} H{H} S{S} Sk{Sk} {pattern}")
     fin = np.isfinite(ref_lse)
     assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
     assert np.all(np.isneginf(lse.cpu().numpy()[~fin]))
 
 
-def test_two_stage_ring_accumulate():
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16])
+def test_two_stage_ring_accumulate(flags):
     # Two KV periods through accumulate + finalize on the two-stage kernel
     # equal one pass over all KV (the K5 merge in its epilogue).
     H, S, d = 3, 1536, 128
@@ -239,7 +241,7 @@ def test_two_stage_ring_accumulate():
     out = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
     half = nb // 2
     for p, ids in enumerate((list(range(half)), list(range(half, nb)))):
-        sc = AttentionSchedule().build(masks, kv_block_ids=ids, kv_tokens_global=S, flags=1 | 8)
+        sc = AttentionSchedule().build(masks, kv_block_ids=ids, kv_tokens_global=S, flags=flags)
         sl = slice(ids[0] * 64, (ids[-1] + 1) * 64)
         sc.launch(qc, kc[sl].contiguous(), vc[sl].contiguous(), out, o_accum=o_acc, lse_accum=l_acc,
                   accumulate=True, finalize=p == 1)
