@@ -359,6 +359,27 @@ typedef struct dbsp_attn_args {
  * built schedule on `stream`.  Uploads the schedule asynchronously. */
 int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* args, void* stream);
 
+/* Fused O return for sequence parallelism: the reverse all-to-all(v) done
+ * in K4's epilogue.  Each bf16 output row (local token t, local head h) is
+ * stored straight into its home rank's output buffer (a peer pointer over
+ * NVLink / NVSwitch, e.g. from CUDA IPC or torch symmetric memory) instead of
+ * the local `o`.  Replaces the separate O exchange of the SP path
+ * (sp.py step 3); SURVEY.md §8(e) "reverse all-to-allv".  All arrays are
+ * device-resident.                                                          */
+typedef struct dbsp_out_scatter {
+  void* const* out_peers;       /* [ranks] bf16 [home_tokens_r, out_heads, d] */
+  const uint32_t* q_block_map;  /* [3 * local Q blocks]: home rank, first home
+                                   row, valid rows of that block              */
+  const uint32_t* head_map;     /* [local heads] -> global head               */
+  uint32_t out_heads;           /* heads of the home buffers (global H)       */
+} dbsp_out_scatter;
+
+/* dbsp_attention_launch with the fused O return: writes go to the home
+ * buffers (`args->o` is not written; it may be NULL).  The default (pair)
+ * schedule and the quad schedules support it. */
+int dbsp_attention_launch_scatter(dbsp_schedule* sched, const dbsp_attn_args* args,
+                                  const dbsp_out_scatter* scatter, void* stream);
+
 /* Convenience: build + launch for a whole single-GPU problem (identity view). */
 int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, void* stream);
 

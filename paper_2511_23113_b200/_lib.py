@@ -101,6 +101,11 @@ class AttnArgsT(C.Structure):
                 ("softmax_scale", f32), ("accumulate", u32), ("finalize", u32)]
 
 
+class OutScatterT(C.Structure):
+    _fields_ = [("out_peers", C.c_void_p), ("q_block_map", C.c_void_p), ("head_map", C.c_void_p),
+                ("out_heads", C.c_uint32)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "dbsp_last_error": (C.c_char_p, []),
@@ -153,6 +158,7 @@ _SIGS = {
     "dbsp_schedule_upload": (C.c_int, [C.c_void_p, C.c_void_p]),
     "dbsp_schedule_upload_bytes": (C.c_int, [C.c_void_p, P(u64)]),
     "dbsp_attention_launch": (C.c_int, [C.c_void_p, P(AttnArgsT), C.c_void_p]),
+    "dbsp_attention_launch_scatter": (C.c_int, [C.c_void_p, P(AttnArgsT), P(OutScatterT), C.c_void_p]),
     "dbsp_sparse_attention": (C.c_int, [P(MaskSetT), P(AttnArgsT), C.c_void_p]),
     "dbsp_accum_init": (C.c_int, [C.c_void_p, C.c_void_p, u32, u32, u32, C.c_void_p]),
     "dbsp_copy_2d": (C.c_int, [C.c_void_p, u64, C.c_void_p, u64, u64, u64, i32, C.c_void_p]),

@@ -112,7 +112,9 @@ class AttentionSchedule:
                *, lse: Optional[torch.Tensor] = None, o_accum: Optional[torch.Tensor] = None,
                lse_accum: Optional[torch.Tensor] = None, accumulate: bool = False,
                finalize: bool = False, softmax_scale: Optional[float] = None,
-               stream: Optional[torch.cuda.Stream] = None) -> None:
+               stream: Optional[torch.cuda.Stream] = None, scatter: Optional["OutScatter"] = None) -> None:
+        """scatter: fused O return -- bf16 rows go to their home ranks' buffers
+        (dbsp_attention_launch_scatter) instead of `out`."""
         for t, n in ((q, "q"), (k, "k"), (v, "v")):
             _require_cuda(t, n)
         if out is not None:
@@ -133,7 +135,37 @@ class AttentionSchedule:
                            lse_accum.data_ptr() if lse_accum is not None else None,
                            Sq, Sk, H, d, float(softmax_scale or 0.0), int(accumulate), int(finalize))
         s = stream if stream is not None else torch.cuda.current_stream(q.device)
+        if scatter is not None:
+            if len(scatter.head_map) != H:
+                raise ContractError("scatter head map must cover the local heads")
+            sc = scatter.c()
+            check(L.lib().dbsp_attention_launch_scatter(self._h, C.byref(args), C.byref(sc),
+                                                        C.c_void_p(s.cuda_stream)))
+            return
         check(L.lib().dbsp_attention_launch(self._h, C.byref(args), C.c_void_p(s.cuda_stream)))
+
+
+class OutScatter:
+    """Device tables of the fused O return (include/dbsp_b200.h dbsp_out_scatter):
+    peer output pointers per rank, per local Q block (home rank, first home
+    row, valid rows) and local -> global heads."""
+
+    def __init__(self, peer_ptrs: Sequence[int], q_block_map: np.ndarray, head_map: Sequence[int],
+                 out_heads: int, device):
+        qm = np.ascontiguousarray(np.asarray(q_block_map, np.int64).reshape(-1, 3))
+        if (qm[:, 0] >= len(peer_ptrs)).any() or (qm < 0).any():
+            raise ContractError("scatter block map addresses past the peer table")
+        hm = np.asarray(head_map, np.int64)
+        if len(hm) and (hm.min() < 0 or hm.max() >= out_heads):
+            raise ContractError("scatter head map addresses past the home heads")
+        self.peers = torch.tensor([int(p) for p in peer_ptrs], dtype=torch.int64, device=device)
+        self.q_map = torch.as_tensor(qm.astype(np.int32).reshape(-1), device=device)
+        self.head_map = torch.as_tensor(hm.astype(np.int32), device=device)
+        self.out_heads = int(out_heads)
+
+    def c(self):
+        return L.OutScatterT(self.peers.data_ptr(), self.q_map.data_ptr(), self.head_map.data_ptr(),
+                             self.out_heads)
 
 
 def accum_init(o_accum: torch.Tensor, lse_accum: torch.Tensor, stream=None) -> None:

@@ -500,8 +500,10 @@ int dbsp_schedule_upload_bytes(const dbsp_schedule* s, uint64_t* bytes) {
   });
 }
 
-int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* stream_ptr) {
-  return guard([&] {
+namespace {
+void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_out_scatter* sc,
+                      void* stream_ptr) {
+  {
     if (!sched || !a) fail(kContract, "null schedule or args");
     if (a->head_dim != 64 && a->head_dim != 128) fail(kConfig, "head_dim must be 64 or 128");
     if (!a->q || !a->k || !a->v) fail(kContract, "null q/k/v");
@@ -510,7 +512,9 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     if (reinterpret_cast<uintptr_t>(a->q) % 16) fail(kContract, "q must be 16-byte aligned");
     const bool acc = a->accumulate != 0;
     if (acc && (!a->o_accum || !a->lse_accum)) fail(kContract, "accumulate needs o_accum/lse_accum");
-    if ((!acc || a->finalize) && !a->o) fail(kContract, "null output");
+    if ((!acc || a->finalize) && !a->o && !sc) fail(kContract, "null output");
+    if (sc && (!sc->out_peers || !sc->q_block_map || !sc->head_map || sc->out_heads == 0))
+      fail(kContract, "incomplete output scatter");
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     const Schedule& h = sched->host;
     const uint32_t n_items = sched->on_device ? sched->dev_items : uint32_t(h.items.size());
@@ -538,11 +542,17 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.trace = g_trace;
     prm.clock_probe = g_clock_probe;
+    prm.out_peers = sc ? reinterpret_cast<__nv_bfloat16* const*>(sc->out_peers) : nullptr;
+    prm.scatter_rows = sc ? sc->q_block_map : nullptr;
+    prm.scatter_heads = sc ? sc->head_map : nullptr;
+    prm.out_heads = sc ? sc->out_heads : 0;
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
     const bool quad = !sched->on_device && (h.flags & kSchedQuad);
     if (quad && use_pair() && a->head_dim != 128) fail(kConfig, "the CTA-pair kernel needs head_dim 128");
+    if (sc && ((quad && use_pair()) || (!quad && (use_wide() || use_split()))))
+      fail(kConfig, "the fused O return is not available in the opt-in pair/wide/split kernels");
     if (quad && use_pair())
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
     else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
@@ -563,6 +573,19 @@ int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* s
       launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
     else
       launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
+  }
+}
+}  // namespace
+
+int dbsp_attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, void* stream) {
+  return guard([&] { attention_launch(sched, a, nullptr, stream); });
+}
+
+int dbsp_attention_launch_scatter(dbsp_schedule* sched, const dbsp_attn_args* a,
+                                  const dbsp_out_scatter* sc, void* stream) {
+  return guard([&] {
+    if (!sc) fail(kContract, "null output scatter");
+    attention_launch(sched, a, sc, stream);
   });
 }
 

@@ -52,7 +52,28 @@ struct AttnParams {
   // Optional: CTA 0 writes {clock64, globaltimer} at start and end, so the host
   // can read the SM clock the kernel actually ran at (power capping).
   unsigned long long* clock_probe;
+  // Fused O return (reverse all-to-all in the epilogue).  Non-null: the bf16
+  // row (local token t, local head h) goes to out_peers[rank] -- the home
+  // rank's [home tokens, out_heads, D] buffer, a peer pointer over NVLink --
+  // at row scatter_rows[3*(t/64)+1] + t%64 and head scatter_heads[h];
+  // scatter_rows[3*b] is the home rank, [3*b+2] the valid rows of block b.
+  __nv_bfloat16* const* out_peers;
+  const uint32_t* scatter_rows;
+  const uint32_t* scatter_heads;
+  uint32_t out_heads;
 };
+
+// Where the bf16 output row of (local token, local head) goes: the local
+// buffer, or its home rank's buffer when the O return is fused (out_peers).
+template <int D>
+__device__ __forceinline__ __nv_bfloat16* out_row_ptr(const AttnParams& p, uint32_t token, uint32_t head,
+                                                     bool& live) {
+  if (p.out_peers == nullptr) return p.out + (size_t(token) * p.heads + head) * D;
+  const uint32_t* e = p.scatter_rows + 3 * (token >> 6);
+  const uint32_t r = token & 63u;
+  live = live && r < e[2];
+  return p.out_peers[e[0]] + (size_t(e[1] + r) * p.out_heads + p.scatter_heads[head]) * D;
+}
 
 __device__ __forceinline__ void clock_probe_mark(const AttnParams& p, int slot) {
   if (p.clock_probe && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -105,6 +126,8 @@ __device__ __forceinline__ void finish_row(const AttnParams& p, uint32_t ocol, b
   const float lse_new = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
   const size_t orow = (size_t(token) * p.heads + head) * D;
   const size_t lidx = size_t(head) * p.q_tokens + token;
+  bool live_out = live;
+  __nv_bfloat16* const orow_ptr = out_row_ptr<D>(p, token, head, live_out);
 
   float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
   const bool acc = (p.mode & kModeAccumulate) != 0;
@@ -156,8 +179,8 @@ __device__ __forceinline__ void finish_row(const AttnParams& p, uint32_t ocol, b
 #pragma unroll
       for (int i = 0; i < 32; ++i) r[i] = __uint_as_float(o[i]) * inv_l;
     }
-    if (write_bf16) {
-      uint4* po = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+    if (write_bf16 && live_out) {
+      uint4* po = reinterpret_cast<uint4*>(orow_ptr + c * 32);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         po[i] = make_uint4(pack_bf16x2(r[8 * i + 0], r[8 * i + 1]),
@@ -172,6 +195,7 @@ __device__ __forceinline__ void finish_row(const AttnParams& p, uint32_t ocol, b
     else if (p.lse)
       p.lse[lidx] = lse_new;
   }
+  if (p.out_peers) __threadfence_system();  // peer stores complete before the kernel ends
 }
 
 template <int D>
@@ -507,6 +531,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const float lse_new = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
     const size_t orow = (size_t(token) * p.heads + it.head) * D;
     const size_t lidx = size_t(it.head) * p.q_tokens + token;
+    bool live_out = live;
+    __nv_bfloat16* const orow_ptr = out_row_ptr<D>(p, token, it.head, live_out);
 
     float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
     const bool acc = (p.mode & kModeAccumulate) != 0;
@@ -558,8 +584,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = __uint_as_float(o[i]) * inv_l;
       }
-      if (write_bf16) {
-        uint4* po = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+      if (write_bf16 && live_out) {
+        uint4* po = reinterpret_cast<uint4*>(orow_ptr + c * 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           po[i] = make_uint4(pack_bf16x2(r[8 * i + 0], r[8 * i + 1]),
@@ -574,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       else if (p.lse)
         p.lse[lidx] = lse_new;
     }
+    if (p.out_peers) __threadfence_system();  // peer stores complete before the kernel ends
   }
 
   tc_fence_before();

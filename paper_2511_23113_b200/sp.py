@@ -117,7 +117,12 @@ class SPAttention:
 
     def __init__(self, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
                  tokens: int, head_dim: int, rank: int, world: int, device, attn_fn: AttnFn = None,
-                 group=None):
+                 group=None, fuse_return: bool = False):
+        """fuse_return: step 3 runs inside K4's epilogue -- every rank's home
+        output shard lives in torch symmetric memory and the final launch
+        stores O rows straight into the home shards over NVLink
+        (dbsp_attention_launch_scatter), so there is no separate O exchange.
+        The CUDA attention path only."""
         if strategy.gpus() != world:
             raise ContractError(f"strategy {strategy} needs {strategy.gpus()} ranks, have {world}")
         if tokens % 64:
@@ -131,8 +136,27 @@ class SPAttention:
         self.me = self.layouts[rank]
         self.xp = exchange_plan(rank, world, self.layouts, self.nb)
         # reverse exchange: what each peer sends back to me / I send back to each home
-        self.attn_fn = attn_fn or _cuda_attn_fn(masks, self.me, tokens)
+        self._symm = None
+        self._scatter = None
+        if fuse_return:
+            if attn_fn is not None:
+                raise ContractError("fuse_return needs the CUDA attention path")
+            self._setup_fused_return(masks.num_heads)
+        self.attn_fn = attn_fn or _cuda_attn_fn(masks, self.me, tokens, self._scatter)
         self._prepare_indices()
+
+    def _setup_fused_return(self, H: int):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        from .attention import OutScatter
+        rows = max(home_range(r, self.world, self.nb)[1] - home_range(r, self.world, self.nb)[0]
+                   for r in range(self.world)) * 64
+        self._home_out = symm.empty(rows, H, self.d, dtype=torch.bfloat16, device=self.device)
+        self._symm = symm.rendezvous(self._home_out, self.group or dist.group.WORLD)
+        peers = [int(ptr) + int(self._symm.offset) for ptr in self._symm.buffer_ptrs]
+        qmap, hmap = scatter_maps(self.me, self.world, self.nb, self.S)
+        self._scatter = OutScatter(peers, qmap, hmap, H, self.device)
 
     # -- index tensors (host -> device once per plan)
     def _prepare_indices(self):
@@ -241,6 +265,22 @@ class SPAttention:
 
         # ---- 3. reverse all-to-all(v): O back to the home layout
         T_home = q_home.shape[0]
+        if self._symm is not None:
+            # Rows already went home in the final launch's epilogue.  A rank
+            # whose last period held no KV block launched nothing: its (merged
+            # or zero) rows go home by peer-tensor copies instead.
+            if len(self.me.kv_groups[self.me.period_groups[y - 1]]) == 0 and nq_loc and Hu:
+                qmap, _ = scatter_maps(self.me, world, self.nb, self.S)
+                hs = torch.as_tensor(self.me.heads, device=dev)
+                for i, (r, row0, _n) in enumerate(qmap):
+                    peer = self._symm.get_buffer(int(r), tuple(self._home_out.shape), dt)
+                    peer[int(row0):int(row0) + 64, hs] = o_loc[i * 64:(i + 1) * 64]
+            self._symm.barrier()
+            res = self._home_out[:T_home]
+            if out_home is None:
+                return res.clone()
+            out_home.copy_(res)
+            return out_home
         if out_home is None:
             out_home = torch.empty(T_home, H, d, device=dev, dtype=dt)
         ops, recvs = [], []
@@ -265,8 +305,9 @@ class SPAttention:
         return out_home
 
 
-def _cuda_attn_fn(masks: AttentionMaskSet, me: RankLayout, tokens: int) -> AttnFn:
-    """K4 per ring period on the local buffers; schedules built once per plan."""
+def _cuda_attn_fn(masks: AttentionMaskSet, me: RankLayout, tokens: int, scatter=None) -> AttnFn:
+    """K4 per ring period on the local buffers; schedules built once per plan.
+    scatter: the final launch returns O to the home shards (fused step 3)."""
     from .attention import AttentionSchedule, accum_init
 
     scheds: Dict[int, AttentionSchedule] = {}
@@ -287,34 +328,53 @@ def _cuda_attn_fn(masks: AttentionMaskSet, me: RankLayout, tokens: int) -> AttnF
             if sc is None:
                 out_loc.zero_()
             else:
-                sc.launch(q_loc, k_buf, v_buf, out_loc)
+                sc.launch(q_loc, k_buf, v_buf, out_loc, scatter=scatter)
             return
         if first:
             accum_init(o_acc, lse_acc)
         if sc is not None:
             sc.launch(q_loc, k_buf, v_buf, out_loc, o_accum=o_acc, lse_accum=lse_acc, accumulate=True,
-                      finalize=last)
+                      finalize=last, scatter=scatter if last else None)
         elif last:
             out_loc.copy_(o_acc.to(out_loc.dtype))
 
     return fn
 
 
+def scatter_maps(layout: RankLayout, world: int, nb: int, tokens: int):
+    """Tables of the fused O return for one rank (dbsp_out_scatter): for each
+    local Q block (ascending global id = local order) its home rank, first row
+    in the home shard and valid rows; and local -> global heads."""
+    starts = np.array([home_range(r, world, nb)[0] for r in range(world)], np.int64)
+    qb = np.asarray(layout.q_blocks, np.int64)
+    home = np.searchsorted(starts, qb, side="right") - 1
+    row0 = (qb - starts[home]) * 64
+    valid = np.minimum(64, tokens - qb * 64)
+    return np.stack([home, row0, valid], axis=1), np.asarray(layout.heads, np.int64)
+
+
 # ----------------------------------------------------------------------------- single-GPU simulation
 def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
-                        time_kernels: bool = True, reps: int = 3):
+                        time_kernels: bool = True, reps: int = 3, fuse_return: bool = False):
     """Run every rank's per-period kernels of UxRy on ONE GPU (no exchange:
     the local buffers are gathered from the global tensors), merge exactly as
     the distributed path does, and time each (rank, period) launch with CUDA
-    events.  Returns (out [S,H,d], times_ms[period][rank])."""
+    events.  fuse_return: the final launch of each rank writes O straight into
+    G separate home-shard buffers through the kernel's scatter epilogue (the
+    fused reverse all-to-all; on one GPU the "peers" are local allocations),
+    and the result is their concatenation.  Returns (out [S,H,d],
+    times_ms[period][rank])."""
     import torch
-    from .attention import AttentionSchedule, accum_init
+    from .attention import AttentionSchedule, OutScatter, accum_init
 
     S, H, d = q.shape
     nb = S // 64
     layouts = rank_layouts(strategy, plan, masks.num_q_blocks, masks.num_kv_blocks)
     y = strategy.ring
     out = torch.zeros_like(q)
+    G = len(layouts)
+    homes = [torch.zeros((home_range(r, G, nb)[1] - home_range(r, G, nb)[0]) * 64, H, d, device=q.device,
+                         dtype=q.dtype) for r in range(G)] if fuse_return else None
     times = [[0.0] * len(layouts) for _ in range(y)]
     for lay in layouts:
         if len(lay.heads) == 0 or len(lay.q_blocks) == 0:
@@ -326,12 +386,21 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
         o_acc = torch.empty(q_loc.shape, device=q.device, dtype=torch.float32)
         lse_acc = torch.empty(len(lay.heads), q_loc.shape[0], device=q.device, dtype=torch.float32)
         accum_init(o_acc, lse_acc)
+        scat = None
+        if fuse_return:
+            qmap, hmap = scatter_maps(lay, G, nb, S)
+            scat = OutScatter([t.data_ptr() for t in homes], qmap, hmap, H, q.device)
         for p in range(y):
             g = lay.period_groups[p]
             kvb = lay.kv_groups[g]
             if len(kvb) == 0:
                 if p == y - 1:
                     o_loc.copy_(o_acc.to(o_loc.dtype)) if y > 1 else o_loc.zero_()
+                    if fuse_return:  # no launch left to carry the return: copy as the NCCL path would
+                        lo = np.asarray([home_range(r, G, nb)[0] for r in range(G)])
+                        for i, b in enumerate(lay.q_blocks):
+                            r = int(np.searchsorted(lo, b, side="right") - 1)
+                            homes[r][(b - lo[r]) * 64:(b - lo[r] + 1) * 64, hs] = o_loc[i * 64:(i + 1) * 64]
                 continue
             kr = torch.as_tensor(_rows(kvb), device=q.device)
             k_loc = k.index_select(0, kr).index_select(1, hs).contiguous()
@@ -356,13 +425,18 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
                     torch.cuda.synchronize()
                     best = min(best, ev[0].elapsed_time(ev[1]))
                 times[p][lay.rank] = best
+            last = p == y - 1
+            sk = scat if last else None
             if y == 1:
-                sc.launch(q_loc, k_loc, v_loc, o_loc)
+                sc.launch(q_loc, k_loc, v_loc, o_loc, scatter=sk)
             else:
                 sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=o_acc, lse_accum=lse_acc, accumulate=True,
-                          finalize=(p == y - 1))
-        out[rows[:, None], hs[None, :]] = o_loc
+                          finalize=last, scatter=sk)
+        if not fuse_return:
+            out[rows[:, None], hs[None, :]] = o_loc
     torch.cuda.synchronize()
+    if fuse_return:
+        out = torch.cat(homes, 0)
     return out, times
 
 
@@ -373,3 +447,66 @@ def measured_rho(times: Sequence[Sequence[float]]) -> float:
     if total == 0:
         return 1.0
     return float(t.max(axis=1).sum() * t.shape[1] / total)
+
+
+def time_ranks_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
+                          scratch=None, reps: int = 1, flags: int = 1):
+    """Kernel times only: every (period, rank) K4 launch of UxRy timed on this
+    GPU without gathering the local buffers.  K4's cost depends on the work
+    list and the buffer footprint, not on the values, so each launch runs on
+    contiguous views [local tokens, local heads, d] carved from flat scratch
+    buffers of the global size (filled once from q/k/v).  Used for long
+    measured sweeps (config E), where the per-call gathers of
+    simulate_on_one_gpu would dominate.  Returns times_ms[period][rank]."""
+    import torch
+    from .attention import AttentionSchedule
+
+    S, H, d = q.shape
+    layouts = rank_layouts(strategy, plan, masks.num_q_blocks, masks.num_kv_blocks)
+    y = strategy.ring
+    if scratch is None:
+        scratch = time_scratch(q, k, v)
+    qf, kf, vf, of, af, lf = scratch
+    times = [[0.0] * len(layouts) for _ in range(y)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for lay in layouts:
+        hl, nq = len(lay.heads), len(lay.q_blocks)
+        if hl == 0 or nq == 0:
+            continue
+        sq = nq * 64
+        q_loc = qf[:sq * hl * d].view(sq, hl, d)
+        o_loc = of[:sq * hl * d].view(sq, hl, d)
+        o_acc = af[:sq * hl * d].view(sq, hl, d)
+        l_acc = lf[:sq * hl].view(hl, sq)
+        for p in range(y):
+            kvb = lay.kv_groups[lay.period_groups[p]]
+            if len(kvb) == 0:
+                continue
+            sk = len(kvb) * 64
+            k_loc = kf[:sk * hl * d].view(sk, hl, d)
+            v_loc = vf[:sk * hl * d].view(sk, hl, d)
+            sc = AttentionSchedule().build(masks, head_ids=lay.heads, q_block_ids=lay.q_blocks,
+                                           kv_block_ids=kvb, kv_tokens_global=S, flags=flags)
+            sc.upload()
+            best = float("inf")
+            for _ in range(reps):
+                ev[0].record()
+                if y == 1:
+                    sc.launch(q_loc, k_loc, v_loc, o_loc)
+                else:
+                    sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=o_acc, lse_accum=l_acc, accumulate=True)
+                ev[1].record()
+                ev[1].synchronize()
+                best = min(best, ev[0].elapsed_time(ev[1]))
+            times[p][lay.rank] = best
+    return times
+
+
+def time_scratch(q, k, v):
+    """Flat scratch buffers for time_ranks_on_one_gpu (values copied from q/k/v)."""
+    import torch
+    S, H, d = q.shape
+    f32 = dict(device=q.device, dtype=torch.float32)
+    return (q.reshape(-1).clone(), k.reshape(-1).clone(), v.reshape(-1).clone(),
+            torch.empty(S * H * d, device=q.device, dtype=q.dtype), torch.zeros(S * H * d, **f32),
+            torch.full((H * S,), float("-inf"), **f32))

@@ -66,7 +66,10 @@ def run_distributed(args, wl, rank: int, world: int):
 
         # per-period kernel timing (events on the compute stream) for a measured rho_s
         times = {}
-        sp = SPAttention(masks, st, plan, S, d, rank, world, dev)
+        # DBSP_FUSE_RETURN=1: O returns home inside K4's epilogue (symmetric
+        # memory peer stores) instead of the NCCL reverse all-to-all(v).
+        fuse = os.environ.get("DBSP_FUSE_RETURN", "0") == "1"
+        sp = SPAttention(masks, st, plan, S, d, rank, world, dev, fuse_return=fuse)
         base_fn = sp.attn_fn
         record = {"on": False}
 
@@ -144,6 +147,7 @@ def run_distributed(args, wl, rank: int, world: int):
             "warmup": args.warmup, "ms_per_step": round(ms_max, 4), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {**wl.describe(), "parallelism": f"sp-{st}", "strategy": str(st),
+                       "o_return": "fused K4 epilogue (symmetric memory)" if fuse else "NCCL all-to-allv",
                        "balance": args.balance, "selector": args.strategy,
                        "l2": "inputs larger than L2 (per-rank shards + exchanged buffers)"},
             "rho_s": round(rho_plan, 4), "rho_s_measured": round(rho_meas, 4),

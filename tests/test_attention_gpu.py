@@ -249,7 +249,8 @@ def test_two_stage_ring_accumulate(flags):
     check(out, ref, "two-stage ring accumulate")
 
 
-def test_nccl_executor_single_rank():
+@pytest.mark.parametrize("fuse_return", [False, True])
+def test_nccl_executor_single_rank(fuse_return):
     # The NCCL-backed executor (the N>1 bench leg) on a 1-rank group: device
     # index tensors, buffers and the K4 launch path through SPAttention.
     import socket
@@ -268,7 +269,8 @@ def test_nccl_executor_single_rank():
         masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.2, 0.5, 1.0, 3))
         q, k, v = (t.cuda() for t in make_qkv(S, H, d, 5))
         st = D.ParallelStrategy(1, 1)
-        sp = SPAttention(masks, st, D.plan_dual(masks, st).plan, S, d, 0, 1, torch.device("cuda"))
+        sp = SPAttention(masks, st, D.plan_dual(masks, st).plan, S, d, 0, 1, torch.device("cuda"),
+                         fuse_return=fuse_return)
         out = sp(q, k, v)
         ref = sparse_attention(q, k, v, masks)
         torch.cuda.synchronize()
@@ -327,3 +329,21 @@ def test_full_size_sampled_rows(name):
     fin = np.isfinite(lr)
     assert np.array_equal(fin, np.isfinite(la))
     assert np.abs(la[fin] - lr[fin]).max() < 1e-2
+
+
+@pytest.mark.parametrize("strategy", ["U8R1", "U4R2", "U2R4", "U1R8"])
+@pytest.mark.parametrize("balanced", [False, True])
+def test_fused_o_return_matches_separate_exchange(strategy, balanced):
+    # The reverse all-to-all fused into K4's epilogue (rows stored straight
+    # into each home shard) gives bit-identical results to running the same
+    # per-rank kernels and moving O separately.
+    from paper_2511_23113_b200.sp import simulate_on_one_gpu
+    H, S, d = 16, 4096, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 21))
+    st = D.parse_strategy(strategy)
+    plan = D.plan_dual(masks, st).plan if balanced else D.default_plan(masks, st)
+    q, k, v = (t.cuda() for t in make_qkv(S, H, d, 22))
+    ref, _ = simulate_on_one_gpu(q, k, v, masks, st, plan, time_kernels=False)
+    got, _ = simulate_on_one_gpu(q, k, v, masks, st, plan, time_kernels=False, fuse_return=True)
+    assert torch.equal(got, ref)
