@@ -308,7 +308,22 @@ def planner_timing(masks, G: int = 8, reps: int = 5, workload: str = None) -> di
     for i in range(reps):
         sel = D.select(i, masks, prof, D.PlannerConfig(), D.SelectorState(G))
     ms = (time.perf_counter() - t0) / reps * 1e3
-    return {"select_ms_per_call": round(ms, 3), "gpus_planned": G, "selected": str(sel.strategy),
+    dev_ms = None
+    try:  # the GPU selector (dbsp_select_device) on device-resident mask words
+        import numpy as np
+        import torch
+        words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).cuda()
+        sd = D.select_device(0, words, masks.num_kv_blocks, prof, D.PlannerConfig(), D.SelectorState(G))
+        assert str(sd.strategy) == str(sel.strategy) and sd.outcome.rho_post == sel.outcome.rho_post
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(reps):
+            D.select_device(i, words, masks.num_kv_blocks, prof, D.PlannerConfig(), D.SelectorState(G))
+        dev_ms = round((time.perf_counter() - t0) / reps * 1e3, 3)
+    except Exception as e:  # reported, never silently replaced
+        dev_ms = f"failed: {e}"
+    return {"select_ms_per_call": round(ms, 3), "select_device_ms_per_call": dev_ms,
+            "gpus_planned": G, "selected": str(sel.strategy),
             "rho_s_post": round(sel.outcome.rho_post, 4),
             "profile": measured.name if workload and measured.exists() else "b200_nominal.json",
             "threads": os.cpu_count()}

@@ -280,6 +280,26 @@ int dbsp_select(dbsp_selector* state, int64_t layer, const dbsp_mask_set* set,
                 dbsp_strategy* strategy_out, dbsp_plan* plan_out,
                 dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out);
 
+/* select() with every mask-dependent integer computed on the GPU from
+ * device-resident mask words (u64 [heads][q_blocks][ceil(kv_blocks/64)], the
+ * BlockMask row layout): K1 head counts and grid marginals, then one kernel
+ * for the workload tables of all (strategy, plan) pairs.  The LPT/greedy
+ * assignments and every double run on the host in the reference's order, so
+ * the result equals dbsp_select bit for bit.
+ * Synchronous on `stream`.  Replaces selector.hpp:55-75 for GPU callers.   */
+int dbsp_select_device(dbsp_selector* state, int64_t layer, const uint64_t* d_words, uint32_t heads,
+                       uint32_t q_blocks, uint32_t kv_blocks, uint32_t block_size,
+                       const dbsp_profile* profile, const dbsp_planner_config* cfg,
+                       dbsp_strategy* strategy_out, dbsp_plan* plan_out,
+                       dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out, void* stream);
+/* The same two-phase selection (assignments first, then one batch of
+ * workload tables) with host tables: CPU check of dbsp_select_device's
+ * planning code.  Results equal dbsp_select.                               */
+int dbsp_select_two_phase(dbsp_selector* state, int64_t layer, const dbsp_mask_set* set,
+                          const dbsp_profile* profile, const dbsp_planner_config* cfg,
+                          dbsp_strategy* strategy_out, dbsp_plan* plan_out,
+                          dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out);
+
 /* ------------------------------------------------------------------------ */
 /* Block-sparse attention on sm_100a (new)          */
 /*

@@ -17,7 +17,8 @@ from .planner import (  # noqa: F401
     generate_mask_set, head_level_imbalance, imbalance_ratio, kInfiniteReward, load_mask_set,
     mix_seed, save_mask_set,
     parse_strategy, partition_blocks, partition_heads, perturb_mask_set, plan_dual,
-    predict_all, predict_from_inputs, predict_latency, select, summed_grid, total_blocks,
+    predict_all, predict_from_inputs, predict_latency, select, select_device, select_two_phase,
+    summed_grid, total_blocks,
     validate_plan, workload_table)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -148,6 +148,11 @@ _SIGS = {
                                    P(StrategyT), P(PlanT), u32, P(PredictionT), P(PlanT), P(u32)]),
     "dbsp_select": (C.c_int, [C.c_void_p, i64, P(MaskSetT), P(ProfileT), P(PlannerConfigT),
                               P(StrategyT), P(PlanT), P(PlanOutcomeT), P(LatencyT)]),
+    "dbsp_select_two_phase": (C.c_int, [C.c_void_p, i64, P(MaskSetT), P(ProfileT), P(PlannerConfigT),
+                                        P(StrategyT), P(PlanT), P(PlanOutcomeT), P(LatencyT)]),
+    "dbsp_select_device": (C.c_int, [C.c_void_p, i64, C.c_void_p, u32, u32, u32, u32, P(ProfileT),
+                                     P(PlannerConfigT), P(StrategyT), P(PlanT), P(PlanOutcomeT), P(LatencyT),
+                                     C.c_void_p]),
     "dbsp_schedule_create": (C.c_int, [P(C.c_void_p)]),
     "dbsp_schedule_destroy": (None, [C.c_void_p]),
     "dbsp_schedule_build": (C.c_int, [C.c_void_p, P(MaskSetT), P(LocalViewT), i32]),

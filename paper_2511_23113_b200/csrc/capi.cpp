@@ -7,6 +7,7 @@
 
 #include "../../include/dbsp_b200.h"
 #include "capi_util.hpp"
+#include "planner_device.hpp"
 #include "core.hpp"
 
 using namespace dbsp_core;
@@ -499,6 +500,61 @@ int dbsp_select(dbsp_selector* state, int64_t layer, const dbsp_mask_set* set,
     if (plan_out) write_plan(p.outcome.plan, plan_out);
     write_outcome(p.outcome, outcome_out);
     write_latency(p.latency, latency_out);
+  });
+}
+
+namespace {
+void write_selection(const Prediction& p, dbsp_strategy* strategy_out, dbsp_plan* plan_out,
+                     dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out) {
+  if (strategy_out) *strategy_out = dbsp_strategy{p.strategy.x, p.strategy.y};
+  if (plan_out) write_plan(p.outcome.plan, plan_out);
+  write_outcome(p.outcome, outcome_out);
+  write_latency(p.latency, latency_out);
+}
+}  // namespace
+
+int dbsp_select_two_phase(dbsp_selector* state, int64_t layer, const dbsp_mask_set* set,
+                          const dbsp_profile* profile, const dbsp_planner_config* cfg,
+                          dbsp_strategy* strategy_out, dbsp_plan* plan_out,
+                          dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out) {
+  return guard([&] {
+    need(state, "selector");
+    const MaskView m = view_of(set);
+    const MaskStats st = mask_stats(m, true);
+    auto host_tables = [&](const std::vector<TableJob>& jobs) {
+      std::vector<Table> t;
+      for (const TableJob& j : jobs)
+        t.push_back(workload_table(m, j.s, j.plan->head.data(), j.plan->q.data(), j.plan->kv.data(), &st));
+      return t;
+    };
+    write_selection(select_batched(state->state, layer, m, st, profile_of(profile), cfg_of(cfg), host_tables),
+                    strategy_out, plan_out, outcome_out, latency_out);
+  });
+}
+
+int dbsp_select_device(dbsp_selector* state, int64_t layer, const uint64_t* d_words, uint32_t heads,
+                       uint32_t q_blocks, uint32_t kv_blocks, uint32_t block_size,
+                       const dbsp_profile* profile, const dbsp_planner_config* cfg,
+                       dbsp_strategy* strategy_out, dbsp_plan* plan_out,
+                       dbsp_plan_outcome* outcome_out, dbsp_latency* latency_out, void* stream) {
+  return guard([&] {
+    need(state, "selector");
+    need(d_words, "device mask words");
+    if (q_blocks == 0 || kv_blocks == 0) fail(kConfig, "BlockMask dimensions must be positive");
+    if (heads == 0) fail(kConfig, "mask set needs at least one head");
+    if (block_size == 0) fail(kConfig, "block_size must be positive");
+    MaskView m;  // dimensions only: every mask-dependent integer comes from the GPU
+    m.H = heads;
+    m.nq = q_blocks;
+    m.nk = kv_blocks;
+    m.block_size = block_size;
+    m.wpr = (size_t(kv_blocks) + 63) / 64;
+    const MaskStats st = dbsp_device_planner::mask_stats(d_words, heads, q_blocks, kv_blocks, stream);
+    auto dev_tables = [&](const std::vector<TableJob>& jobs) {
+      return dbsp_device_planner::workload_tables(d_words, m, st, jobs, stream);
+    };
+    write_selection(select_batched(state->state, layer, m, st, profile_of(profile), cfg_of(cfg), dev_tables),
+                    strategy_out, plan_out, outcome_out, latency_out);
   });
 }
 

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 namespace dbsp_core {
@@ -225,6 +226,16 @@ class Selector {
   mutable std::mutex mu_;
   std::map<int64_t, std::pair<Strategy, Plan>> prev_;
 };
+// One workload table per (strategy, plan) job; see select_batched.
+struct TableJob {
+  Strategy s;
+  const Plan* plan;
+};
+using BatchTables = std::function<std::vector<Table>(const std::vector<TableJob>&)>;
+void plan_assign(const MaskView& m, Strategy s, const PlannerConfig& cfg, const Plan* prev,
+                 const MaskStats* st, Outcome& out);
+Prediction select_batched(Selector& state, int64_t layer, const MaskView& m, const MaskStats& st,
+                          const Profile& p, const PlannerConfig& cfg, const BatchTables& tables);
 Prediction select(Selector& state, int64_t layer, const MaskView& m, const Profile& p,
                   const PlannerConfig& cfg);
 

@@ -486,27 +486,13 @@ void partition_blocks(const MaskView& m, uint32_t y, double reward, const MaskSt
   kv_out = biased_greedy(st->col_weights.data(), m.nk, y, reward);
 }
 
-// planner.hpp:175-217 (Alg. 1).
-Outcome plan_dual(const MaskView& m, Strategy s, const PlannerConfig& cfg, const Plan* prev,
-                  const MaskStats* st, Table* post_table) {
-  cfg.validate();
+// Alg. 1's assignment steps (planner.hpp:195-214) without the two workload
+// tables: head plan reused or re-packed, block plan always recomputed.  Only
+// head counts and grid marginals are read, so a caller that evaluates the
+// tables elsewhere (on the GPU, select_batched) gets the same plan.
+void plan_assign(const MaskView& m, Strategy s, const PlannerConfig& cfg, const Plan* prev,
+                 const MaskStats* st, Outcome& out) {
   const uint32_t x = s.x, y = s.y;
-  if (prev) {
-    if (prev->head.size() != m.H || prev->q.size() != m.nq || prev->kv.size() != m.nk)
-      fail(kContract, "plan dimensions do not match the mask set");
-    validate_plan(m, s, prev->head.data(), prev->q.data(), prev->kv.data());
-  }
-  Outcome out;
-  {
-    Plan dflt;
-    const Plan* pre = prev;
-    if (!pre) {
-      dflt = default_plan(m, s);
-      pre = &dflt;
-    }
-    out.rho_pre = imbalance_ratio(
-        workload_table(m, s, pre->head.data(), pre->q.data(), pre->kv.data(), st));
-  }
   if (x > 1) {
     bool reuse = false;
     if (prev) {
@@ -529,6 +515,35 @@ Outcome plan_dual(const MaskView& m, Strategy s, const PlannerConfig& cfg, const
     out.plan.q.assign(m.nq, 0);
     out.plan.kv.assign(m.nk, 0);
   }
+}
+
+namespace {
+void check_prev(const MaskView& m, Strategy s, const Plan* prev) {
+  if (prev) {
+    if (prev->head.size() != m.H || prev->q.size() != m.nq || prev->kv.size() != m.nk)
+      fail(kContract, "plan dimensions do not match the mask set");
+    validate_plan(m, s, prev->head.data(), prev->q.data(), prev->kv.data());
+  }
+}
+}  // namespace
+
+// planner.hpp:175-217 (Alg. 1).
+Outcome plan_dual(const MaskView& m, Strategy s, const PlannerConfig& cfg, const Plan* prev,
+                  const MaskStats* st, Table* post_table) {
+  cfg.validate();
+  check_prev(m, s, prev);
+  Outcome out;
+  {
+    Plan dflt;
+    const Plan* pre = prev;
+    if (!pre) {
+      dflt = default_plan(m, s);
+      pre = &dflt;
+    }
+    out.rho_pre = imbalance_ratio(
+        workload_table(m, s, pre->head.data(), pre->q.data(), pre->kv.data(), st));
+  }
+  plan_assign(m, s, cfg, prev, st, out);
   Table post = workload_table(m, s, out.plan.head.data(), out.plan.q.data(),
                               out.plan.kv.data(), st);
   out.rho_post = imbalance_ratio(post);
@@ -859,6 +874,59 @@ Prediction select(Selector& state, int64_t layer, const MaskView& m, const Profi
   Plan plan;
   if (state.stored(layer, s, plan)) prev.emplace(s, std::move(plan));
   std::vector<Prediction> all = predict_all(m, p, state.gpus(), cfg, prev);
+  size_t best = 0;
+  for (size_t i = 1; i < all.size(); ++i)
+    if (all[i].latency.total < all[best].latency.total) best = i;
+  state.store(layer, all[best].strategy, all[best].outcome.plan);
+  return std::move(all[best]);
+}
+
+// select() with the mask-dependent integers supplied from outside: `st`
+// (head counts, grid marginals) and the workload tables (`tables`, one call
+// for every (strategy, plan) pair of the selection).  Used by the device path
+// (dbsp_select_device), where K1 and a table kernel produce them on the GPU;
+// `m` then carries dimensions only.  Plans, doubles and the argmin follow the
+// same code as select(), so the result is identical to the host path.
+Prediction select_batched(Selector& state, int64_t layer, const MaskView& m, const MaskStats& st,
+                          const Profile& p, const PlannerConfig& cfg, const BatchTables& tables) {
+  cfg.validate();
+  std::map<Strategy, Plan> prev;
+  {
+    Strategy s;
+    Plan plan;
+    if (state.stored(layer, s, plan)) prev.emplace(s, std::move(plan));
+  }
+  std::vector<Strategy> feasible;
+  for (Strategy s : enumerate_strategies(state.gpus()))
+    if (s.x <= m.H && s.y <= std::min(m.nq, m.nk)) feasible.push_back(s);
+  if (feasible.empty())
+    fail(kConfig, "no feasible strategy for " + str(state.gpus()) + " GPUs on this mask shape");
+  std::vector<Prediction> all(feasible.size());
+  std::vector<Plan> pre(feasible.size());
+  std::vector<TableJob> jobs;
+  for (size_t i = 0; i < feasible.size(); ++i) {
+    const Strategy s = feasible[i];
+    const auto it = prev.find(s);
+    const Plan* pv = it != prev.end() ? &it->second : nullptr;
+    check_prev(m, s, pv);
+    pre[i] = pv ? *pv : default_plan(m, s);
+    all[i].strategy = s;
+    plan_assign(m, s, cfg, pv, &st, all[i].outcome);
+    validate_plan(m, s, all[i].outcome.plan.head.data(), all[i].outcome.plan.q.data(),
+                  all[i].outcome.plan.kv.data());
+  }
+  for (size_t i = 0; i < feasible.size(); ++i) {
+    jobs.push_back({feasible[i], &pre[i]});
+    jobs.push_back({feasible[i], &all[i].outcome.plan});
+  }
+  const std::vector<Table> t = tables(jobs);
+  if (t.size() != jobs.size()) fail(kInternal, "table provider returned the wrong count");
+  for (size_t i = 0; i < feasible.size(); ++i) {
+    all[i].outcome.rho_pre = imbalance_ratio(t[2 * i]);
+    all[i].outcome.rho_post = imbalance_ratio(t[2 * i + 1]);
+    all[i].latency = predict_latency(m, feasible[i], all[i].outcome.plan, p, false, &st,
+                                     &all[i].outcome.rho_post);
+  }
   size_t best = 0;
   for (size_t i = 1; i < all.size(); ++i)
     if (all[i].latency.total < all[best].latency.total) best = i;

@@ -798,3 +798,42 @@ def select(layer_id: int, mset: AttentionMaskSet, profile: MachineProfile,
     return Selection(ParallelStrategy(s.ulysses, s.ring),
                      PlanOutcome(plan, bool(oc.head_replanned), oc.rho_pre, oc.rho_post),
                      LatencyBreakdown.of(lat))
+
+
+def select_two_phase(layer_id: int, mset: AttentionMaskSet, profile: MachineProfile,
+                     config: PlannerConfig, state: SelectorState) -> Selection:
+    """select() through the two-phase path of select_device (assignments, then
+    one batch of workload tables), tables on the host.  Same result as select()."""
+    s = L.StrategyT()
+    plan = PartitionPlan.empty(mset)
+    oc = L.PlanOutcomeT()
+    lat = L.LatencyT()
+    pc = profile.c()
+    check(L.lib().dbsp_select_two_phase(state._h, layer_id, C.byref(mset.c()), C.byref(pc),
+                                        C.byref(config.c()), C.byref(s), C.byref(plan.c()), C.byref(oc),
+                                        C.byref(lat)))
+    return Selection(ParallelStrategy(s.ulysses, s.ring),
+                     PlanOutcome(plan, bool(oc.head_replanned), oc.rho_pre, oc.rho_post),
+                     LatencyBreakdown.of(lat))
+
+
+def select_device(layer_id: int, words, num_kv_blocks: int, profile: MachineProfile, config: PlannerConfig,
+                  state: SelectorState, block_size: int = 64, stream=None) -> Selection:
+    """select() with the mask integers computed on the GPU (dbsp_select_device).
+    words: contiguous CUDA int64 tensor [H, Nq, ceil(Nk/64)] of BlockMask rows."""
+    import torch
+    if not words.is_cuda or words.dtype != torch.int64 or words.dim() != 3 or not words.is_contiguous():
+        raise ContractError("device mask words must be a contiguous CUDA int64 [H, Nq, words] tensor")
+    H, nq, _ = words.shape
+    s = L.StrategyT()
+    plan = PartitionPlan(np.zeros(H, np.uint32), np.zeros(nq, np.uint32), np.zeros(num_kv_blocks, np.uint32))
+    oc = L.PlanOutcomeT()
+    lat = L.LatencyT()
+    pc = profile.c()
+    st = stream if stream is not None else torch.cuda.current_stream(words.device)
+    check(L.lib().dbsp_select_device(state._h, layer_id, C.c_void_p(words.data_ptr()), H, nq, num_kv_blocks,
+                                     block_size, C.byref(pc), C.byref(config.c()), C.byref(s),
+                                     C.byref(plan.c()), C.byref(oc), C.byref(lat), C.c_void_p(st.cuda_stream)))
+    return Selection(ParallelStrategy(s.ulysses, s.ring),
+                     PlanOutcome(plan, bool(oc.head_replanned), oc.rho_pre, oc.rho_post),
+                     LatencyBreakdown.of(lat))

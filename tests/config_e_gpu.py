@@ -51,6 +51,7 @@ def main():
     st_uni = D.parse_strategy(best_uniform)
 
     state = D.SelectorState(G)
+    host_state = D.SelectorState(G)
     hist = collections.Counter()
     rec = {"dbsp_ms": [], "uniform_ms": [], "rho_dbsp": [], "rho_uniform": [], "select_ms": [],
            "modelled_comm_ms": [], "replans": 0}
@@ -59,9 +60,14 @@ def main():
             if step > 0 and flip > 0:
                 cur[layer] = D.perturb_mask_set(cur[layer], flip, D.mix_seed(base.seed, layer, step))
             m = cur[layer]
+            # the GPU selector on the live mask words (H2D of the words included)
             t0 = time.perf_counter()
-            sel = D.select(layer, m, profile, D.PlannerConfig(), state)
+            words = torch.from_numpy(np.ascontiguousarray(m.words).view(np.int64)).cuda()
+            sel = D.select_device(layer, words, m.num_kv_blocks, profile, D.PlannerConfig(), state)
             rec["select_ms"].append((time.perf_counter() - t0) * 1e3)
+            if step < 2:  # the host selector agrees bit for bit
+                ref = D.select(layer, m, profile, D.PlannerConfig(), host_state)
+                assert str(ref.strategy) == str(sel.strategy) and ref.latency == sel.latency
             hist[str(sel.strategy)] += 1
             rec["replans"] += int(sel.outcome.head_replanned)
             lat = sel.latency
@@ -86,7 +92,8 @@ def main():
         "rho_s_measured": {"dbsp_mean": round(float(a["rho_dbsp"].mean()), 4),
                            "dbsp_max": round(float(a["rho_dbsp"].max()), 4),
                            "uniform_mean": round(float(a["rho_uniform"].mean()), 4)},
-        "select_ms_per_call": {"mean": round(float(a["select_ms"].mean()), 3),
+        "select_ms_per_call": {"path": "dbsp_select_device (checked equal to the host select on the first 2 steps)",
+                               "mean": round(float(a["select_ms"].mean()), 3),
                                "p95": round(float(np.percentile(a["select_ms"], 95)), 3)},
         "modelled_comm_ms_mean": round(float(a["modelled_comm_ms"].mean()), 4),
         "note": "kernel times measured per (period, rank) on one B200; communication not measured "

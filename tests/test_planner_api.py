@@ -2,6 +2,7 @@
 restated against the product planner through the Python face of the C ABI,
 plus error-class behaviour (error.hpp) and the C ABI surface itself."""
 import ctypes
+import json
 import math
 import re
 from pathlib import Path
@@ -314,3 +315,36 @@ def test_selector_no_feasible_strategy():
     m = D.generate_mask_set(D.GeneratorSpec(1, 1, 1, 64, "random", 0.5, 0.5, 1.0, 3))
     with pytest.raises(D.ConfigError, match="no feasible strategy"):
         D.predict_all(m, flat_profile(), 8)
+
+
+def _same_selection(a, b):
+    assert (a.strategy.ulysses, a.strategy.ring) == (b.strategy.ulysses, b.strategy.ring)
+    for x, y in ((a.outcome.plan.head_assignment, b.outcome.plan.head_assignment),
+                 (a.outcome.plan.q_assignment, b.outcome.plan.q_assignment),
+                 (a.outcome.plan.kv_assignment, b.outcome.plan.kv_assignment)):
+        assert np.array_equal(x, y)
+    assert a.outcome.head_replanned == b.outcome.head_replanned
+    # doubles compared exactly (selector.hpp:67-69 argmin on exact totals)
+    assert a.outcome.rho_pre == b.outcome.rho_pre and a.outcome.rho_post == b.outcome.rho_post
+    assert a.latency == b.latency
+
+
+@pytest.mark.parametrize("shape", [(8, 64, 64, "random", 0.5, 0.5), (40, 512, 512, "clustered", 0.15, 0.45),
+                                   (48, 278, 278, "clustered", 0.15, 0.484), (12, 100, 37, "banded", 0.2, 0.7)])
+def test_two_phase_select_equals_select(shape):
+    # The planning code of the device selector (assignments first, then one
+    # batch of workload tables) reproduces select() bit for bit, including
+    # the P_s head-plan reuse across a perturbed chain of calls.
+    H, nq, nk, pat, lo, hi = shape
+    prof = D.MachineProfile.from_json(json.loads(
+        (ROOT / "paper_2511_23113_b200" / "profiles" / "b200_wan_measured.json").read_text()))
+    m = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, pat, lo, hi, 1.0, 3))
+    for gpus in (2, 4, 8):
+        s_host, s_two = D.SelectorState(gpus), D.SelectorState(gpus)
+        cur = m
+        for step in range(4):
+            if step:
+                cur = D.perturb_mask_set(cur, 0.02, D.mix_seed(3, gpus, step))
+            for layer in (0, 1):
+                _same_selection(D.select(layer, cur, prof, D.PlannerConfig(), s_host),
+                                D.select_two_phase(layer, cur, prof, D.PlannerConfig(), s_two))
