@@ -15,6 +15,7 @@
 
 #include "attn_kernel.cuh"
 #include "attn_kernel_duo.cuh"
+#include "attn_kernel_duo2.cuh"
 #include "attn_kernel_quad.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
@@ -193,6 +194,20 @@ void launch_duo(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v
   cuda_check(attr_err, "cudaFuncSetAttribute(duo)");
   dbsp_dev::sparse_attn_fwd_duo_kernel<D><<<items, dbsp_dev::kThreadsDuo, C::kSmemBytes, stream>>>(q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo launch");
+}
+
+void launch_duo2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::Duo2Cfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo2_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(duo2)");
+  dbsp_dev::sparse_attn_fwd_duo2_kernel<<<items, dbsp_dev::kThreadsDuo2, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo2 launch");
 }
 
 template <int D>
@@ -555,7 +570,10 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       fail(kConfig, "the fused O return is not available in the opt-in pair/wide/split kernels");
     if (quad && use_pair())
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
-    else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
+    else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
+      if (a->head_dim != 128) fail(kConfig, "the split-softmax two-stage kernel needs head_dim 128");
+      launch_duo2(tq, tk, tv, prm, n_items, stream);
+    } else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
       launch_duo<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad && (h.flags & kSchedKey128))
       launch_duo<64>(tq, tk, tv, prm, n_items, stream);
