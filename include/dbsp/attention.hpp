@@ -10,6 +10,7 @@
 #include "../dbsp_b200.h"
 #include "error.hpp"
 #include "mask.hpp"
+#include "metrics.hpp"
 
 namespace dbsp {
 
@@ -64,6 +65,39 @@ inline void sparse_attention(const AttentionMaskSet& set, const AttentionArgs& a
   const dbsp_attn_args c{a.q, a.k, a.v, a.o, a.lse, nullptr, nullptr, a.q_tokens, a.kv_tokens,
                          a.heads, a.head_dim, a.softmax_scale, 0, 0};
   detail::check(dbsp_sparse_attention(v.get(), &c, stream));
+}
+
+// The sequence-parallel call: one context per GPU process
+// owns the NCCL communicator; rank 0 makes the id, every rank passes it in.
+class SpContext {
+ public:
+  static std::vector<uint8_t> unique_id() {
+    std::vector<uint8_t> id(128);
+    detail::check(dbsp_nccl_unique_id(id.data(), uint32_t(id.size())));
+    return id;
+  }
+  SpContext(uint32_t rank, uint32_t world, const std::vector<uint8_t>& nccl_id) {
+    detail::check(dbsp_sp_context_create(rank, world, nccl_id.data(), &h_));
+  }
+  ~SpContext() { dbsp_sp_context_destroy(h_); }
+  SpContext(const SpContext&) = delete;
+  SpContext& operator=(const SpContext&) = delete;
+  dbsp_sp_context* handle() const { return h_; }
+
+ private:
+  dbsp_sp_context* h_ = nullptr;
+};
+
+// q/k/v/o: this rank's home shards, bf16 [home tokens, H, d] (rank g holds
+// blocks [g*nb/G, (g+1)*nb/G)); stream-ordered.
+inline void sparse_attention(SpContext& ctx, const AttentionMaskSet& set, ParallelStrategy strategy,
+                             const PartitionPlan& plan, const void* q, const void* k, const void* v, void* o,
+                             uint32_t head_dim, void* stream) {
+  detail::MaskView mv(set);
+  std::vector<uint32_t> h = plan.head_assignment, qa = plan.q_assignment, kv = plan.kv_assignment;
+  const dbsp_plan cp{h.data(), qa.data(), kv.data()};
+  detail::check(dbsp_sp_attention(ctx.handle(), mv.get(), dbsp_strategy{strategy.ulysses, strategy.ring}, &cp,
+                                  q, k, v, o, set.num_q_blocks() * set.block_size(), head_dim, stream));
 }
 
 }  // namespace dbsp

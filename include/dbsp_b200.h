@@ -415,6 +415,30 @@ int dbsp_accum_init(float* o_accum, float* lse_accum, uint32_t q_tokens, uint32_
                     uint32_t head_dim, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Sequence-parallel attention call (SpContext +
+ * sparse_attention).  One process per GPU; the context owns the NCCL
+ * communicator (ncclCommInitRank over `nccl_id`, the ncclUniqueId bytes rank 0
+ * obtained from dbsp_nccl_unique_id) and a communication stream.  Home layout:
+ * rank g holds token blocks [floor(g*nb/G), floor((g+1)*nb/G)) of Q, K, V, O
+ * with all heads, bf16 [home tokens, H, d].  One call = fused all-to-all(v)
+ * (Ulysses head scatter + db-SP balancing moves), y ring periods of K4 with the
+ * KV exchange on the communication stream, reverse all-to-all(v) of O.       */
+typedef struct dbsp_sp_context dbsp_sp_context;
+int dbsp_nccl_unique_id(uint8_t* out, uint32_t size /* >= 128 */);
+int dbsp_sp_context_create(uint32_t rank, uint32_t world, const uint8_t* nccl_id, dbsp_sp_context** out);
+void dbsp_sp_context_destroy(dbsp_sp_context* ctx);
+int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strategy strategy,
+                      const dbsp_plan* plan, const void* q_home, const void* k_home, const void* v_home,
+                      void* o_home, uint32_t tokens, uint32_t head_dim, void* stream);
+/* The same call for all G = x*y ranks on this one GPU, device copies as the
+ * transport: *_homes[g] are rank g's home shards.  Tests the multi-rank
+ * layouts, packing and ring rotation without a second GPU.                  */
+int dbsp_sp_attention_simulated(const dbsp_mask_set* set, dbsp_strategy strategy, const dbsp_plan* plan,
+                                const void* const* q_homes, const void* const* k_homes,
+                                const void* const* v_homes, void* const* o_homes, uint32_t tokens,
+                                uint32_t head_dim, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Mask statistics on device (K1).  Masks are device u64
  * words [H][Nq][ceil(Nk/64)].  Outputs are exact integers.                  */
 int dbsp_mask_stats_device(const uint64_t* d_words, uint32_t heads, uint32_t nq, uint32_t nk,

@@ -153,6 +153,13 @@ _SIGS = {
     "dbsp_select_device": (C.c_int, [C.c_void_p, i64, C.c_void_p, u32, u32, u32, u32, P(ProfileT),
                                      P(PlannerConfigT), P(StrategyT), P(PlanT), P(PlanOutcomeT), P(LatencyT),
                                      C.c_void_p]),
+    "dbsp_nccl_unique_id": (C.c_int, [C.c_void_p, u32]),
+    "dbsp_sp_context_create": (C.c_int, [u32, u32, C.c_void_p, P(C.c_void_p)]),
+    "dbsp_sp_context_destroy": (None, [C.c_void_p]),
+    "dbsp_sp_attention": (C.c_int, [C.c_void_p, P(MaskSetT), StrategyT, P(PlanT), C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, u32, u32, C.c_void_p]),
+    "dbsp_sp_attention_simulated": (C.c_int, [P(MaskSetT), StrategyT, P(PlanT), C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, u32, u32, C.c_void_p]),
     "dbsp_schedule_create": (C.c_int, [P(C.c_void_p)]),
     "dbsp_schedule_destroy": (None, [C.c_void_p]),
     "dbsp_schedule_build": (C.c_int, [C.c_void_p, P(MaskSetT), P(LocalViewT), i32]),

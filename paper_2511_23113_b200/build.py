@@ -20,7 +20,7 @@ BUILD = ROOT / "build" / "dbsp_b200"
 LIB = PKG / "libdbsp_b200.so"
 
 CXX_SOURCES = ["planner_core.cpp", "schedule.cpp", "capi.cpp", "mask_io.cpp"]
-CU_SOURCES = ["attention.cu", "schedule_device.cu", "planner_device.cu"]
+CU_SOURCES = ["attention.cu", "schedule_device.cu", "planner_device.cu", "sp_exec.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 
@@ -77,7 +77,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc, GENCODE, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lcuda"]
+        cmd = [nvcc, GENCODE, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lnccl", "-lcuda"]
         if verbose:
             print(" ".join(cmd))
         try:

@@ -510,3 +510,70 @@ def time_scratch(q, k, v):
     return (q.reshape(-1).clone(), k.reshape(-1).clone(), v.reshape(-1).clone(),
             torch.empty(S * H * d, device=q.device, dtype=q.dtype), torch.zeros(S * H * d, **f32),
             torch.full((H * S,), float("-inf"), **f32))
+
+
+# ----------------------------------------------------------------------------- C++ executor (C ABI)
+class NativeSPContext:
+    """The C-ABI sequence-parallel call (csrc/sp_exec.cu): NCCL communicator,
+    fused all-to-all(v), ring periods of K4 with the KV exchange on a
+    communication stream, reverse all-to-all(v) -- all in C++.  One per
+    process/GPU; rank 0's NCCL id reaches the others through `broadcast_id`
+    (e.g. torch.distributed.broadcast_object_list)."""
+
+    def __init__(self, rank: int, world: int, broadcast_id: Callable[[bytes], bytes]):
+        import ctypes as C
+        from . import _lib as L
+        from .planner import check
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(L.lib().dbsp_nccl_unique_id(C.cast(buf, C.c_void_p), 128))
+        uid = broadcast_id(bytes(buf) if rank == 0 else b"")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(L.lib().dbsp_sp_context_create(rank, world, C.cast(buf, C.c_void_p), C.byref(h)))
+        self._h = h
+        self.rank, self.world = rank, world
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            from . import _lib as L
+            L.lib().dbsp_sp_context_destroy(h)
+            self._h = None
+
+    def __call__(self, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
+                 q_home, k_home, v_home, out_home=None, stream=None):
+        import ctypes as C
+        import torch
+        from . import _lib as L
+        from .planner import check
+        S = masks.num_q_blocks * 64
+        d = q_home.shape[2]
+        if out_home is None:
+            out_home = torch.empty_like(q_home)
+        st = stream if stream is not None else torch.cuda.current_stream(q_home.device)
+        check(L.lib().dbsp_sp_attention(self._h, C.byref(masks.c()), L.StrategyT(strategy.ulysses, strategy.ring),
+                                        C.byref(plan.c()), C.c_void_p(q_home.data_ptr()),
+                                        C.c_void_p(k_home.data_ptr()), C.c_void_p(v_home.data_ptr()),
+                                        C.c_void_p(out_home.data_ptr()), S, d, C.c_void_p(st.cuda_stream)))
+        return out_home
+
+
+def native_sp_simulated(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan):
+    """dbsp_sp_attention_simulated: all G ranks of the C++ executor on this GPU
+    (device copies as the transport).  q/k/v: global [S, H, d]; returns O [S, H, d]."""
+    import ctypes as C
+    import torch
+    from . import _lib as L
+    from .planner import check
+    S, H, d = q.shape
+    nb = S // 64
+    G = strategy.gpus()
+    sl = [slice(home_range(g, G, nb)[0] * 64, home_range(g, G, nb)[1] * 64) for g in range(G)]
+    qs, ks, vs = ([t[s].contiguous() for s in sl] for t in (q, k, v))
+    os_ = [torch.empty_like(x) for x in qs]
+    arr = lambda ts: (C.c_void_p * G)(*[t.data_ptr() for t in ts])
+    check(L.lib().dbsp_sp_attention_simulated(C.byref(masks.c()), L.StrategyT(strategy.ulysses, strategy.ring),
+                                              C.byref(plan.c()), arr(qs), arr(ks), arr(vs), arr(os_), S, d,
+                                              C.c_void_p(torch.cuda.current_stream(q.device).cuda_stream)))
+    return torch.cat(os_, 0)

@@ -4,6 +4,7 @@
 // criteria that need no simulator (proj/tests/acceptance.cpp c1-c6, c8, c9)
 // plus the error behaviour of the reference unit tests.  Prints one line per
 // check; exit code = number of failures.
+#include "dbsp/attention.hpp"  // SpContext / sparse_attention: compiled and linked, not run (no GPU)
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -85,6 +86,13 @@ static MachineProfile node() {
 }
 
 int main() {
+  {  // the attention faces link (their calls need a GPU and are exercised from Python)
+    volatile auto uid = &dbsp::SpContext::unique_id;
+    void (*sp)(dbsp::SpContext&, const dbsp::AttentionMaskSet&, dbsp::ParallelStrategy, const dbsp::PartitionPlan&,
+               const void*, const void*, const void*, void*, uint32_t, void*) = &dbsp::sparse_attention;
+    (void)uid;
+    (void)sp;
+  }
   // c1: rho fixtures.
   {
     WorkloadTable a{2, {{3, 1}, {2, 2}}}, b{2, {{4, 0}}}, c{2, {{5, 5}, {7, 7}}};
