@@ -439,7 +439,9 @@ def main():
             print(json.dumps(res), flush=True)
         return
 
-    if world > 1:
+    # DBSP_BENCH_SP=1 runs the N>1 leg on a 1-rank group (exercises the
+    # distributed executors on one GPU; not a bench line of record)
+    if world > 1 or os.environ.get("DBSP_BENCH_SP") == "1":
         from paper_2511_23113_b200.sp_bench import run_distributed
         res = run_distributed(args, wl, rank, world)
     else:

@@ -82,10 +82,25 @@ def run_distributed(args, wl, rank: int, world: int):
             e1.record()
             times.setdefault(period, []).append((e0, e1))
         sp.attn_fn = timed_fn
+        # DBSP_SP_NATIVE=1: the timed call is the C++ executor (csrc/sp_exec.cu,
+        # dbsp_sp_attention); the per-period instrumentation below still runs
+        # the Python executor, which issues the same kernels.
+        native = os.environ.get("DBSP_SP_NATIVE", "0") == "1"
+        if native:
+            from .sp import NativeSPContext
+
+            def bcast(b):
+                obj = [b]
+                dist.broadcast_object_list(obj, src=0)
+                return obj[0]
+            nctx = NativeSPContext(rank, world, bcast)
+            call = lambda qq, kk, vv, oo=None: nctx(masks, st, plan, qq, kk, vv, oo)
+        else:
+            call = sp
 
         out = torch.empty_like(qh)
         for _ in range(args.warmup):
-            sp(qh, kh, vh, out)
+            call(qh, kh, vh, out)
         torch.cuda.synchronize()
         dist.barrier()
         from bench import ClockSampler, peaks
@@ -94,7 +109,7 @@ def run_distributed(args, wl, rank: int, world: int):
             torch.cuda.synchronize()
             ev0.record()
             for _ in range(args.steps):
-                sp(qh, kh, vh, out)
+                call(qh, kh, vh, out)
             ev1.record()
             torch.cuda.synchronize()
         dist.barrier()
@@ -128,7 +143,7 @@ def run_distributed(args, wl, rank: int, world: int):
         e0.record()
         for _ in range(e2e_steps):
             dq, dk, dv = (x.to(dev, non_blocking=True) for x in (hq, hk, hv))
-            ho.copy_(sp(dq, dk, dv), non_blocking=True)
+            ho.copy_(call(dq, dk, dv), non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
@@ -148,6 +163,7 @@ def run_distributed(args, wl, rank: int, world: int):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {**wl.describe(), "parallelism": f"sp-{st}", "strategy": str(st),
                        "o_return": "fused K4 epilogue (symmetric memory)" if fuse else "NCCL all-to-allv",
+                       "executor": "C++ (dbsp_sp_attention)" if native else "Python (sp.SPAttention)",
                        "balance": args.balance, "selector": args.strategy,
                        "l2": "inputs larger than L2 (per-rank shards + exchanged buffers)"},
             "rho_s": round(rho_plan, 4), "rho_s_measured": round(rho_meas, 4),
