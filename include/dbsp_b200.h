@@ -439,6 +439,31 @@ int dbsp_sp_attention_simulated(const dbsp_mask_set* set, dbsp_strategy strategy
                                 uint32_t head_dim, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* K6: QKV projection with the sequence-parallel all-to-all(v) fused into its
+ * epilogue.  Y = X W^T (+ bias) on one rank's home
+ * tokens, tcgen05 bf16 GEMM with fp32 accumulation; without `scatter` Y is
+ * written to `out` [tokens, 3*H*d]; with it every 32-column row segment of Q
+ * (K, V) goes straight into the local Q (K, V) buffer of the rank that
+ * consumes it under the plan -- the buffers of dbsp_sp_attention's step 1. */
+typedef struct dbsp_qkv_args {
+  const void* x;     /* bf16 [tokens, hidden] (home tokens)                   */
+  const void* w;     /* bf16 [3*heads*head_dim, hidden] (nn.Linear weight)    */
+  const void* bias;  /* bf16 [3*heads*head_dim] or NULL                      */
+  void* out;         /* bf16 [tokens, 3*heads*head_dim] when not scattering  */
+  uint32_t tokens, hidden, heads, head_dim;
+} dbsp_qkv_args;
+typedef struct dbsp_qkv_scatter {
+  void* const* q_peers;       /* [G] device array: rank -> local Q buffer [nq_loc*64, Hu, d]   */
+  void* const* k_peers;       /* [G] rank -> local K buffer of its period-0 group              */
+  void* const* v_peers;       /* [G]                                                           */
+  const uint32_t* block_map;  /* [4 * home blocks]: Q ring rank, Q local block, KV group, KV local block */
+  const uint32_t* head_map;   /* [2 * heads]: Ulysses rank u, local head index                 */
+  const uint32_t* heads_of;   /* [G]: local head count of each rank                            */
+  uint32_t ring;              /* y                                                              */
+} dbsp_qkv_scatter;
+int dbsp_qkv_project(const dbsp_qkv_args* args, const dbsp_qkv_scatter* scatter /* or NULL */, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Mask statistics on device (K1).  Masks are device u64
  * words [H][Nq][ceil(Nk/64)].  Outputs are exact integers.                  */
 int dbsp_mask_stats_device(const uint64_t* d_words, uint32_t heads, uint32_t nq, uint32_t nk,

@@ -101,6 +101,16 @@ class AttnArgsT(C.Structure):
                 ("softmax_scale", f32), ("accumulate", u32), ("finalize", u32)]
 
 
+class QkvArgsT(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("w", C.c_void_p), ("bias", C.c_void_p), ("out", C.c_void_p),
+                ("tokens", u32), ("hidden", u32), ("heads", u32), ("head_dim", u32)]
+
+
+class QkvScatterT(C.Structure):
+    _fields_ = [("q_peers", C.c_void_p), ("k_peers", C.c_void_p), ("v_peers", C.c_void_p),
+                ("block_map", C.c_void_p), ("head_map", C.c_void_p), ("heads_of", C.c_void_p), ("ring", u32)]
+
+
 class OutScatterT(C.Structure):
     _fields_ = [("out_peers", C.c_void_p), ("q_block_map", C.c_void_p), ("head_map", C.c_void_p),
                 ("out_heads", C.c_uint32)]
@@ -153,6 +163,7 @@ _SIGS = {
     "dbsp_select_device": (C.c_int, [C.c_void_p, i64, C.c_void_p, u32, u32, u32, u32, P(ProfileT),
                                      P(PlannerConfigT), P(StrategyT), P(PlanT), P(PlanOutcomeT), P(LatencyT),
                                      C.c_void_p]),
+    "dbsp_qkv_project": (C.c_int, [P(QkvArgsT), C.c_void_p, C.c_void_p]),
     "dbsp_nccl_unique_id": (C.c_int, [C.c_void_p, u32]),
     "dbsp_sp_context_create": (C.c_int, [u32, u32, C.c_void_p, P(C.c_void_p)]),
     "dbsp_sp_context_destroy": (None, [C.c_void_p]),

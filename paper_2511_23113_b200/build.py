@@ -20,7 +20,7 @@ BUILD = ROOT / "build" / "dbsp_b200"
 LIB = PKG / "libdbsp_b200.so"
 
 CXX_SOURCES = ["planner_core.cpp", "schedule.cpp", "capi.cpp", "mask_io.cpp"]
-CU_SOURCES = ["attention.cu", "schedule_device.cu", "planner_device.cu", "sp_exec.cu"]
+CU_SOURCES = ["attention.cu", "schedule_device.cu", "planner_device.cu", "sp_exec.cu", "qkv_proj.cu"]
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 
