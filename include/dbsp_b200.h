@@ -336,7 +336,8 @@ void dbsp_schedule_destroy(dbsp_schedule* sched);
 enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4,
        DBSP_SCHED_QUAD = 8 /* 4 Q blocks per item: two 128-row tiles per CTA sharing one KV stream */,
        DBSP_SCHED_KEY128 = 16 /* with QUAD: 128-key steps (two KV blocks per tcgen05 QK^T) */,
-       DBSP_SCHED_SPLIT_SOFTMAX = 32 /* with QUAD|KEY128, d=128: two softmax warps per row */ };
+       DBSP_SCHED_SPLIT_SOFTMAX = 32 /* with QUAD|KEY128, d=128: two softmax warps per row */,
+       DBSP_SCHED_PERSIST = 64 /* with QUAD, d=128: persistent quad kernel */ };
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
                         const dbsp_local_view* view, int32_t flags);

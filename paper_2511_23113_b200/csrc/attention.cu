@@ -17,6 +17,7 @@
 #include "attn_kernel_duo.cuh"
 #include "attn_kernel_duo2.cuh"
 #include "attn_kernel_quad.cuh"
+#include "attn_kernel_quadp.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
@@ -210,6 +211,25 @@ void launch_duo2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& 
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo2 launch");
 }
 
+void launch_quadp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::QuadPCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int sms = 148;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_quadp_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(quadp)");
+  const uint32_t grid = std::min<uint32_t>(items, uint32_t(sms));  // one persistent CTA per SM
+  dbsp_dev::sparse_attn_fwd_quadp_kernel<<<grid, dbsp_dev::kThreadsQuadP, C::kSmemBytes, stream>>>(q, k, v, prm,
+                                                                                                  items);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_quadp launch");
+}
+
 template <int D>
 void launch_quad(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
@@ -271,6 +291,7 @@ struct dbsp_schedule {
   size_t view_bytes = 0;
   void* k2_scratch = nullptr;
   size_t k2_scratch_bytes = 0;
+  unsigned int* item_counter = nullptr;  // persistent kernels: zeroed before each launch
 
   ~dbsp_schedule() {
     if (pending && uploaded) cudaEventSynchronize(uploaded);
@@ -279,6 +300,7 @@ struct dbsp_schedule {
     if (uploaded) cudaEventDestroy(uploaded);
     if (view_dev) cudaFree(view_dev);
     if (k2_scratch) cudaFree(k2_scratch);
+    if (item_counter) cudaFree(item_counter);
   }
 };
 
@@ -561,6 +583,7 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
     prm.scatter_rows = sc ? sc->q_block_map : nullptr;
     prm.scatter_heads = sc ? sc->head_map : nullptr;
     prm.out_heads = sc ? sc->out_heads : 0;
+    prm.item_counter = nullptr;
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
@@ -577,6 +600,13 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       launch_duo<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad && (h.flags & kSchedKey128))
       launch_duo<64>(tq, tk, tv, prm, n_items, stream);
+    else if (quad && (h.flags & kSchedPersist) && a->head_dim == 128) {
+      if (!sched->item_counter)
+        cuda_check(cudaMalloc(&sched->item_counter, sizeof(unsigned int)), "cudaMalloc item counter");
+      cuda_check(cudaMemsetAsync(sched->item_counter, 0, sizeof(unsigned int), stream), "memset item counter");
+      prm.item_counter = sched->item_counter;
+      launch_quadp(tq, tk, tv, prm, n_items, stream);
+    }
     else if (quad && a->head_dim == 128)
       launch_quad<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad)

@@ -61,6 +61,8 @@ struct AttnParams {
   const uint32_t* scatter_rows;
   const uint32_t* scatter_heads;
   uint32_t out_heads;
+  // Persistent kernels: work-item counter, zeroed before each launch.
+  unsigned int* item_counter;
 };
 
 // Where the bf16 output row of (local token, local head) goes: the local

@@ -56,6 +56,7 @@ constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all head
 constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
 constexpr uint32_t kSchedQuad = 8;       // four Q blocks per item (two-stage kernels)
 constexpr uint32_t kSchedKey128 = 16;    // with kSchedQuad: 128-key steps (attn_kernel_duo.cuh)
+constexpr uint32_t kSchedPersist = 64;  // with kSchedQuad, d=128: persistent quad kernel (attn_kernel_quadp.cuh)
 constexpr uint32_t kSchedSplitSoftmax = 32;  // with kSchedQuad|kSchedKey128, d=128: attn_kernel_duo2.cuh
 // Quad items: WorkItem{head, q0, q1, begin, count, pad_mask, q2, q3}; entries
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
