@@ -153,6 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 2)
         }
         tc_commit_pair(bKempty(s), 0x3);
         tc_commit_pair(bSfull(int(j & 1)), 0x3);
+        DBSP_TR(kTrMmaS, j);
       };
       auto issue_pv = [&](uint32_t i) {
         const int b = int(i & 1);
@@ -168,6 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 2)
         }
         tc_commit_pair(bVempty(s), 0x3);
         tc_commit_pair(bOdone, 0x3);
+        DBSP_TR(kTrMmaPV, i);
       };
       mbar_wait(bQ, 0);
       tc_fence_after();
@@ -199,6 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 2)
       const uint32_t scol = tmem + lane_off + C::kColS + 64u * b;
       mbar_wait(bSfull(b), (j >> 1) & 1);
       tc_fence_after();
+      if (lane == 0 && warp == 0) DBSP_TR(rank ? kTrSoftStartHi : kTrSoftStart, j);
       uint32_t pk[32];
       if (dense) {
         uint32_t sa[32], sb[32];
@@ -269,6 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 2)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if (lane == 0 && warp == 0) DBSP_TR(rank ? kTrSoftEndHi : kTrSoftEnd, j);
       if (lane == 0) {
         if (rank == 0)
           mbar_arrive(bPfull(b));

@@ -45,6 +45,8 @@ def main():
     torch.cuda.synchronize()
     tr = buf.view(B, T, E).cpu().numpy().astype(np.int64)
     fn(None)
+    if os.environ.get("DBSP_K4_PAIR") == "1":  # CTA-pair kernel: default-kernel event layout
+        sched_flags &= ~8
     if sched_flags & 8 and fine:
         fine_report(tr)
         subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
