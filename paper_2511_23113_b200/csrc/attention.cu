@@ -18,6 +18,7 @@
 #include "attn_kernel_duo2.cuh"
 #include "attn_kernel_quad.cuh"
 #include "attn_kernel_quadp.cuh"
+#include "attn_kernel_s32.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
@@ -255,6 +256,29 @@ bool use_pair() {
     return e && e[0] == '1';
   }();
   return pair;
+}
+
+void launch_s32(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm, uint32_t items,
+                cudaStream_t stream) {
+  using C = dbsp_dev::S32Cfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_s32_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(s32)");
+  dbsp_dev::sparse_attn_fwd_s32_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_s32 launch");
+}
+
+// d=128 with Q in TMEM and 32-key sub-steps (attn_kernel_s32.cuh), opt-in.
+bool use_s32() {
+  static const bool s32 = [] {
+    const char* e = std::getenv("DBSP_K4_S32");
+    return e && e[0] == '1';
+  }();
+  return s32;
 }
 
 // d=128 kernel choice.  The 128-key-step variant (one CTA/SM) measured 6.96 ms
@@ -611,6 +635,8 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       launch_quad<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad)
       launch_quad<64>(tq, tk, tv, prm, n_items, stream);
+    else if (a->head_dim == 128 && use_s32())
+      launch_s32(tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128 && use_wide())
       launch_wide(tk, tv, prm, n_items, stream);
     else if (use_split() && a->head_dim == 128)

@@ -6,6 +6,7 @@ oracle.  Inputs are the bf16-rounded Q/K/V, so the comparison measures the
 kernel's arithmetic, not input quantisation.
 """
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -383,3 +384,32 @@ def test_native_sp_context_nccl_single_rank():
     ref = sparse_attention(q, k, v, masks)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_s32_kernel_subprocess():
+    # The Q-in-TMEM, 32-key sub-step d=128 kernel (DBSP_K4_S32=1, read once
+    # per process) on ragged, partial and rescale-heavy cases, in a child.
+    import subprocess
+    import sys
+    code = r"""
+import sys; sys.path.insert(0, %r)
+import numpy as np, torch, oracle, paper_2511_23113_b200 as D
+from paper_2511_23113_b200.attention import sparse_attention
+for (H, S, Sk, pat, seed) in [(4, 2048, 2048, "clustered", 1), (3, 1000, 1990, "random", 2), (2, 700, 700, "banded", 3)]:
+    nq, nk = -(-S // 64), -(-Sk // 64)
+    m = D.generate_mask_set(D.GeneratorSpec(H, nq, nk, 64, pat, 0.15, 0.6, 1.0, seed))
+    g = torch.Generator().manual_seed(seed)
+    q = (torch.randn(S, H, 128, generator=g) * 3).to(torch.bfloat16)
+    k, v = (torch.randn(Sk, H, 128, generator=g).to(torch.bfloat16) for _ in range(2))
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(), m.words, nk)
+    out, lse = sparse_attention(q.cuda(), k.cuda(), v.cuda(), m, return_lse=True)
+    o = out.float().cpu().numpy()
+    mx = float(np.abs(o - ref).max()); rel = float(np.linalg.norm(o - ref) / np.linalg.norm(ref))
+    assert mx <= 2e-2 and rel <= 1e-2, (mx, rel)
+    fin = np.isfinite(ref_lse)
+    assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+print("ok")
+""" % str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       env={**__import__("os").environ, "DBSP_K4_S32": "1"})
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
