@@ -44,7 +44,7 @@ class AttentionSchedule:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and L is not None:  # modules may be gone at interpreter exit
             L.lib().dbsp_schedule_destroy(h)
             self._h = None
 
