@@ -348,3 +348,54 @@ def test_two_phase_select_equals_select(shape):
             for layer in (0, 1):
                 _same_selection(D.select(layer, cur, prof, D.PlannerConfig(), s_host),
                                 D.select_two_phase(layer, cur, prof, D.PlannerConfig(), s_two))
+
+
+def test_new_entry_points_validate_before_touching_the_gpu():
+    # The C ABI of the GPU paths checks its arguments on the host and fails
+    # with the reference's error classes (error.hpp:10-44) before any CUDA call.
+    L = _lib.lib()
+    C = ctypes
+    # K6: head_dim 96, then 3*H*d not a multiple of 256, then a null input
+    a = _lib.QkvArgsT(1, 1, None, 1, 128, 512, 4, 96)
+    assert L.dbsp_qkv_project(C.byref(a), None, None) == 2
+    a = _lib.QkvArgsT(1, 1, None, 1, 128, 512, 1, 64)
+    assert L.dbsp_qkv_project(C.byref(a), None, None) == 2
+    a = _lib.QkvArgsT(None, 1, None, 1, 128, 512, 4, 64)
+    assert L.dbsp_qkv_project(C.byref(a), None, None) == 4
+    # the fused scatter needs whole 64-token blocks and a complete table set
+    a = _lib.QkvArgsT(1, 1, None, None, 100, 512, 4, 64)
+    sc = _lib.QkvScatterT(1, 1, 1, 1, 1, 1, 1)
+    assert L.dbsp_qkv_project(C.byref(a), C.byref(sc), None) == 4
+    # GPU selector: null words / zero dims
+    st = D.SelectorState(4)
+    prof = D.MachineProfile.from_json(json.loads(
+        (ROOT / "paper_2511_23113_b200" / "profiles" / "b200_nominal.json").read_text()))
+    out = [_lib.StrategyT(), None, _lib.PlanOutcomeT(), _lib.LatencyT()]
+    rc = L.dbsp_select_device(st._h, 0, None, 4, 8, 8, 64, C.byref(prof.c()), C.byref(D.PlannerConfig().c()),
+                              C.byref(out[0]), None, C.byref(out[2]), C.byref(out[3]), None)
+    assert rc == 4
+    rc = L.dbsp_select_device(st._h, 0, C.c_void_p(8), 4, 0, 8, 64, C.byref(prof.c()),
+                              C.byref(D.PlannerConfig().c()), C.byref(out[0]), None, C.byref(out[2]),
+                              C.byref(out[3]), None)
+    assert rc == 2
+    # C++ SP call: strategy / rank-count mismatch and bad plans, before any NCCL or CUDA work
+    m = D.generate_mask_set(D.GeneratorSpec(4, 8, 8, 64, "random", 0.5, 0.5, 1.0, 1))
+    plan = D.default_plan(m, D.ParallelStrategy(2, 2))
+    ptrs = (C.c_void_p * 4)(1, 1, 1, 1)
+    rc = L.dbsp_sp_attention_simulated(C.byref(m.c()), _lib.StrategyT(2, 2), C.byref(plan.c()), ptrs, ptrs, ptrs,
+                                       ptrs, 8 * 64, 96, None)
+    assert rc == 2  # head_dim
+    rc = L.dbsp_sp_attention_simulated(C.byref(m.c()), _lib.StrategyT(2, 2), C.byref(plan.c()), ptrs, ptrs, ptrs,
+                                       ptrs, 8 * 64 - 1, 64, None)
+    assert rc == 4  # tokens must be whole blocks
+    bad = D.PartitionPlan.of([0, 0, 1, 3], plan.q_assignment, plan.kv_assignment)
+    rc = L.dbsp_sp_attention_simulated(C.byref(m.c()), _lib.StrategyT(2, 2), C.byref(bad.c()), ptrs, ptrs, ptrs,
+                                       ptrs, 8 * 64, 64, None)
+    assert rc == 4  # head assigned past x
+    # fused O return: incomplete scatter tables
+    sc2 = _lib.OutScatterT(None, 1, 1, 4)
+    sched = C.c_void_p()
+    assert L.dbsp_schedule_create(C.byref(sched)) == 0
+    args = _lib.AttnArgsT(1, 1, 1, None, None, None, None, 64, 64, 4, 64, 0.0, 0, 0)
+    assert L.dbsp_attention_launch_scatter(sched, C.byref(args), C.byref(sc2), None) == 4
+    L.dbsp_schedule_destroy(sched)
