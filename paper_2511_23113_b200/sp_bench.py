@@ -51,6 +51,10 @@ def run_distributed(args, wl, rank: int, world: int):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
+    # A collective over all ranks first: batch_isend_irecv as the first NCCL
+    # call of a group must involve every rank, which the ragged exchanges
+    # need not do.
+    dist.barrier()
     try:
         masks = P.generate_mask_set(wl.spec())
         st, plan = choose(masks, world, args.strategy, args.balance, args.workload)
