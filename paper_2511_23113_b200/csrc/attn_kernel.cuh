@@ -428,8 +428,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     const float sl2 = p.scale_log2;
     const uint32_t* ent = p.entries + it.begin;
     float m = -INFINITY, l = 0.f;
+    // Entries are read one step ahead: when S_j is already waiting, the
+    // global load of entry j would otherwise sit on the softmax chain.
+    uint32_t e_next = count > 0 ? __ldg(ent) : 0u;
     for (uint32_t j = 0; j < count; ++j) {
+#ifndef DBSP_NO_ENTRY_PREFETCH
+      const uint32_t e = e_next;
+      if (j + 1 < count) e_next = __ldg(ent + j + 1);
+#else
       const uint32_t e = __ldg(ent + j);
+#endif
       const bool dense = (e & dense_bit) != 0;  // warp-uniform (one half per warp)
       const int b = int(j % NSB);
       const uint32_t scol = tmem + lane_off + C::kColS + 64u * b;
