@@ -413,3 +413,33 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        env={**__import__("os").environ, "DBSP_K4_S32": "1"})
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("flags", [1, 1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64])
+def test_empty_heads_rows_and_quads_every_kernel(flags):
+    # An all-empty head, empty Q rows, a whole empty quad (count 0 work items)
+    # and a fully dense head, through every kernel family; rows without a
+    # dense tile give O = 0 and LSE = -inf.
+    H, S, d = 4, 1536, 128
+    nq = nk = S // 64
+    rng = np.random.default_rng(3)
+    dense = rng.random((H, nq, nk)) < 0.4
+    dense[0] = False                 # empty head
+    dense[1, 4:8, :] = False         # an empty quad of Q blocks in head 1
+    dense[1, 10, :] = False          # one empty Q row
+    dense[2] = True                  # fully dense head
+    masks = D.AttentionMaskSet.from_dense(dense)
+    q, k, v = make_qkv(S, H, d, 10)
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                           masks.words, nk)
+    sc = AttentionSchedule().build(masks, kv_tokens_global=S, flags=flags)
+    out = torch.full((S, H, d), 7.0, device="cuda", dtype=torch.bfloat16)  # garbage must be overwritten
+    lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
+    sc.launch(q.cuda(), k.cuda(), v.cuda(), out, lse=lse)
+    torch.cuda.synchronize()
+    check(out, ref, f"empty/dense flags {flags}")
+    assert torch.all(out[:, 0] == 0) and torch.all(torch.isneginf(lse[0]))
+    assert torch.all(out[4 * 64:8 * 64, 1] == 0) and torch.all(out[10 * 64:11 * 64, 1] == 0)
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
+    assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
