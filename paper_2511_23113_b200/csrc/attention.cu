@@ -19,6 +19,7 @@
 #include "attn_kernel_quad.cuh"
 #include "attn_kernel_quadp.cuh"
 #include "attn_kernel_s32.cuh"
+#include "attn_kernel_psmem.cuh"
 #include "attn_kernel_pair.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
@@ -270,6 +271,29 @@ void launch_s32(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::Attn
   cuda_check(attr_err, "cudaFuncSetAttribute(s32)");
   dbsp_dev::sparse_attn_fwd_s32_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_s32 launch");
+}
+
+void launch_psmem(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm,
+                  uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::PsmemCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_psmem_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(psmem)");
+  dbsp_dev::sparse_attn_fwd_psmem_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_psmem launch");
+}
+
+// d=128 with P staged in smem (attn_kernel_psmem.cuh), opt-in.
+bool use_psmem() {
+  static const bool on = [] {
+    const char* e = std::getenv("DBSP_K4_PSMEM");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 // d=128 with Q in TMEM and 32-key sub-steps (attn_kernel_s32.cuh), opt-in.
@@ -635,6 +659,8 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       launch_quad<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad)
       launch_quad<64>(tq, tk, tv, prm, n_items, stream);
+    else if (a->head_dim == 128 && use_psmem())
+      launch_psmem(tq, tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128 && use_s32())
       launch_s32(tk, tv, prm, n_items, stream);
     else if (a->head_dim == 128 && use_wide())

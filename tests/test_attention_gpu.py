@@ -386,7 +386,8 @@ def test_native_sp_context_nccl_single_rank():
     assert torch.equal(out, ref)
 
 
-def test_s32_kernel_subprocess():
+@pytest.mark.parametrize("env", ["DBSP_K4_S32", "DBSP_K4_PSMEM"])
+def test_optin_d128_kernels_subprocess(env):
     # The Q-in-TMEM, 32-key sub-step d=128 kernel (DBSP_K4_S32=1, read once
     # per process) on ragged, partial and rescale-heavy cases, in a child.
     import subprocess
@@ -411,7 +412,7 @@ for (H, S, Sk, pat, seed) in [(4, 2048, 2048, "clustered", 1), (3, 1000, 1990, "
 print("ok")
 """ % str(Path(__file__).resolve().parents[1])
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
-                       env={**__import__("os").environ, "DBSP_K4_S32": "1"})
+                       env={**__import__("os").environ, env: "1"})
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
