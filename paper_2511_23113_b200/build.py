@@ -77,7 +77,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         objs.append(obj)
     if force or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc, GENCODE, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lnccl", "-lcuda"]
+        cmd = [nvcc, GENCODE, "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-ldl", "-lcuda"]
         if verbose:
             print(" ".join(cmd))
         try:

@@ -21,9 +21,12 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -33,6 +36,52 @@
 
 using namespace dbsp_core;
 using dbsp_capi::guard;
+
+namespace {
+
+// NCCL is resolved at run time (dlopen of libnccl.so.2) rather than linked: a
+// process that already loaded torch's bundled NCCL gets that same library
+// back, so there is never a second NCCL in the process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& N() {
+  static NcclApi api;
+  static std::string err;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load NCCL: ") + dlerror();
+      return;
+    }
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn && err.empty()) err = std::string("NCCL symbol missing: ") + name;
+    };
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.Send, "ncclSend");
+    sym(api.Recv, "ncclRecv");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.GetErrorString, "ncclGetErrorString");
+  });
+  if (!err.empty()) dbsp_core::fail(dbsp_core::kCuda, err);
+  return api;
+}
+
+}  // namespace
 
 namespace dbsp_dev {
 // dst[(i*nh + j)*d + c] = src[row(i)*H*d + heads[j]*d + c], row(i) = (blocks[i/64] - lo)*64 + i%64.
@@ -71,7 +120,7 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
 }
 void nck(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) fail(kCuda, std::string(what) + ": " + ncclGetErrorString(r));
+  if (r != ncclSuccess) fail(kCuda, std::string(what) + ": " + N().GetErrorString(r));
 }
 void rc(int code) {
   if (code != 0) fail(code, dbsp_last_error());
@@ -399,7 +448,7 @@ struct dbsp_sp_context {
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_done = nullptr;
   std::unique_ptr<RankExec> ex;
   ~dbsp_sp_context() {
-    if (comm) ncclCommDestroy(comm);
+    if (comm) N().CommDestroy(comm);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     for (cudaEvent_t e : ev_ready)
       if (e) cudaEventDestroy(e);
@@ -442,7 +491,7 @@ int dbsp_nccl_unique_id(uint8_t* out, uint32_t size) {
   return guard([&] {
     if (!out || size < sizeof(ncclUniqueId)) fail(kContract, "unique id buffer too small");
     ncclUniqueId id;
-    nck(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    nck(N().GetUniqueId(&id), "ncclGetUniqueId");
     std::memcpy(out, &id, sizeof(id));
   });
 }
@@ -454,7 +503,7 @@ int dbsp_sp_context_create(uint32_t rank, uint32_t world, const uint8_t* nccl_id
     auto ctx = std::make_unique<dbsp_sp_context>();
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
-    nck(ncclCommInitRank(&ctx->comm, int(world), id, int(rank)), "ncclCommInitRank");
+    nck(N().CommInitRank(&ctx->comm, int(world), id, int(rank)), "ncclCommInitRank");
     ctx->rank = rank;
     ctx->world = world;
     ck(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking), "comm stream");
@@ -487,7 +536,7 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
     const uint32_t G = ctx->world, me = ctx->rank;
     // 1. fused all-to-all(v) on the compute stream (it gates everything after it)
     E.pack_forward(q_home, k_home, v_home, st);
-    nck(ncclGroupStart(), "group");
+    nck(N().GroupStart(), "group");
     for (uint32_t x = 0; x < G; ++x) {
       const size_t bq = E.piece_bytes(x, E.send_q_h[x].size()), bkv = E.piece_bytes(x, E.send_kv_h[x].size());
       uint8_t* qd = static_cast<uint8_t*>(E.q_loc.p) + E.q_off(x);
@@ -502,18 +551,18 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
         }
         continue;
       }
-      if (bq) nck(ncclSend(E.sendq[x].p, bq, ncclUint8, int(x), ctx->comm, st), "send q");
+      if (bq) nck(N().Send(E.sendq[x].p, bq, ncclUint8, int(x), ctx->comm, st), "send q");
       if (bkv) {
-        nck(ncclSend(E.sendk[x].p, bkv, ncclUint8, int(x), ctx->comm, st), "send k");
-        nck(ncclSend(E.sendv[x].p, bkv, ncclUint8, int(x), ctx->comm, st), "send v");
+        nck(N().Send(E.sendk[x].p, bkv, ncclUint8, int(x), ctx->comm, st), "send k");
+        nck(N().Send(E.sendv[x].p, bkv, ncclUint8, int(x), ctx->comm, st), "send v");
       }
-      if (rq) nck(ncclRecv(qd, rq, ncclUint8, int(x), ctx->comm, st), "recv q");
+      if (rq) nck(N().Recv(qd, rq, ncclUint8, int(x), ctx->comm, st), "recv q");
       if (rkv) {
-        nck(ncclRecv(kd, rkv, ncclUint8, int(x), ctx->comm, st), "recv k");
-        nck(ncclRecv(vd, rkv, ncclUint8, int(x), ctx->comm, st), "recv v");
+        nck(N().Recv(kd, rkv, ncclUint8, int(x), ctx->comm, st), "recv k");
+        nck(N().Recv(vd, rkv, ncclUint8, int(x), ctx->comm, st), "recv v");
       }
     }
-    nck(ncclGroupEnd(), "group");
+    nck(N().GroupEnd(), "group");
     // 2. ring periods: K4 on the held group while the next one arrives on the comm stream
     const Layout& L = E.me;
     const uint32_t y = L.y;
@@ -525,16 +574,16 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
         const size_t nn = L.groups[L.period_group(pd + 1)].size() * 64 * E.row_bytes;
         ck(cudaEventRecord(ctx->ev_ready[cur], st), "event");  // the held group is in place
         ck(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready[cur], 0), "wait");
-        nck(ncclGroupStart(), "group");
+        nck(N().GroupStart(), "group");
         if (n && E.row_bytes) {
-          nck(ncclSend(E.kbuf[cur].p, n, ncclUint8, int(prv), ctx->comm, ctx->comm_stream), "ring send k");
-          nck(ncclSend(E.vbuf[cur].p, n, ncclUint8, int(prv), ctx->comm, ctx->comm_stream), "ring send v");
+          nck(N().Send(E.kbuf[cur].p, n, ncclUint8, int(prv), ctx->comm, ctx->comm_stream), "ring send k");
+          nck(N().Send(E.vbuf[cur].p, n, ncclUint8, int(prv), ctx->comm, ctx->comm_stream), "ring send v");
         }
         if (nn && E.row_bytes) {
-          nck(ncclRecv(E.kbuf[1 - cur].p, nn, ncclUint8, int(nxt), ctx->comm, ctx->comm_stream), "ring recv k");
-          nck(ncclRecv(E.vbuf[1 - cur].p, nn, ncclUint8, int(nxt), ctx->comm, ctx->comm_stream), "ring recv v");
+          nck(N().Recv(E.kbuf[1 - cur].p, nn, ncclUint8, int(nxt), ctx->comm, ctx->comm_stream), "ring recv k");
+          nck(N().Recv(E.vbuf[1 - cur].p, nn, ncclUint8, int(nxt), ctx->comm, ctx->comm_stream), "ring recv v");
         }
-        nck(ncclGroupEnd(), "group");
+        nck(N().GroupEnd(), "group");
       }
       E.compute(pd, cur, st);
       if (pd + 1 < y) {
@@ -544,7 +593,7 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
       cur = 1 - cur;
     }
     // 3. reverse all-to-all(v): O slices go home, then land in the home layout
-    nck(ncclGroupStart(), "group");
+    nck(N().GroupStart(), "group");
     for (uint32_t x = 0; x < G; ++x) {
       const size_t sb = size_t(E.oslice_n[x]) * 64 * E.row_bytes;
       const size_t rb = size_t(E.back_blocks[x].n) * 64 * E.all[x].heads.size() * head_dim * 2;
@@ -552,10 +601,10 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
         if (sb) ck(cudaMemcpyAsync(E.recvo[x].p, E.oslice(x), sb, cudaMemcpyDeviceToDevice, st), "self o");
         continue;
       }
-      if (sb) nck(ncclSend(E.oslice(x), sb, ncclUint8, int(x), ctx->comm, st), "send o");
-      if (rb) nck(ncclRecv(E.recvo[x].p, rb, ncclUint8, int(x), ctx->comm, st), "recv o");
+      if (sb) nck(N().Send(E.oslice(x), sb, ncclUint8, int(x), ctx->comm, st), "send o");
+      if (rb) nck(N().Recv(E.recvo[x].p, rb, ncclUint8, int(x), ctx->comm, st), "recv o");
     }
-    nck(ncclGroupEnd(), "group");
+    nck(N().GroupEnd(), "group");
     E.unpack_reverse(o_home, st);
   });
 }
