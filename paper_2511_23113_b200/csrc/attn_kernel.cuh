@@ -209,18 +209,24 @@ struct KCfg {
   // room for only one S buffer next to the 128-col O, which serialises
   // softmax and MMA inside a CTA (measured 1.24x slower than Q in smem with
   // two S buffers), so Q stays in smem (SS-mode QK^T) there.
+#ifdef DBSP_D64_QSMEM3
+  // d=64 alternative: Q in smem frees 32 TMEM columns for a third S buffer.
+  static constexpr bool kQInTmem = false;
+  static constexpr int kNSB = D == 64 ? 3 : 2;
+#else
   static constexpr bool kQInTmem = D == 64;
+  static constexpr int kNSB = 2;
+#endif
   static constexpr uint32_t kQBytes = kQInTmem ? 0u : 128u * D * 2u;
   static constexpr uint32_t kQChunk = 128u * 128u;  // one 64-column chunk of a 128-row Q tile
   // TMEM columns (256 per CTA): [Q], NSB S/P buffers of 64 cols, O (fp32, D
   // cols); regions 64-column aligned.
-  static constexpr int kNSB = 2;
   static constexpr uint32_t kColQ = 0;
   static constexpr uint32_t kColS = kQInTmem ? 64 : 0;
   static constexpr uint32_t kColO = kColS + 64 * kNSB;
   static_assert(kColO + D <= kTmemCols, "TMEM budget");
-  static constexpr int kStages = D == 128 ? 2 : 6;  // K/V smem ring depth
-  static constexpr int kNumBars = 4 * kStages + 2 * kNSB + 3;
+  static constexpr int kStages = D == 128 ? 2 : (kQInTmem ? 6 : 5);  // K/V smem ring depth
+  static constexpr int kNumBars = 4 * kStages + 2 * kNSB + 4;
   static constexpr uint32_t kDataBytes = kQBytes + 2u * kStages * kTileBytes;
   static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
 };
@@ -249,8 +255,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   auto bSfull = [&](int b) { return sBar + 8u * (4 * NS + b); };
   auto bPfull = [&](int b) { return sBar + 8u * (4 * NS + NSB + b); };
   const uint32_t bQready = sBar + 8u * (4 * NS + 2 * NSB);      // Q in TMEM / smem
-  const uint32_t bOdone = sBar + 8u * (4 * NS + 2 * NSB + 1);   // one phase per PV_j
-  const uint32_t bOfinal = sBar + 8u * (4 * NS + 2 * NSB + 2);  // single phase: all PVs done
+  // PV_j commits bOdone(j & 1): with NSB=3, S_j completes after PV_{j-3}, so
+  // two PVs may be pending and a single barrier's parity would alias.
+  auto bOdone = [&](uint32_t j) { return sBar + 8u * (4 * NS + 2 * NSB + 1 + (j & 1)); };
+  const uint32_t bOfinal = sBar + 8u * (4 * NS + 2 * NSB + 3);  // single phase: all PVs done
   const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
 
   const int warp = threadIdx.x >> 5;
@@ -275,7 +283,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(bPfull(b), 4);  // one arrive per softmax warp
     }
     mbar_init(bQready, C::kQInTmem ? 4 : 1);  // 4 softmax warps, or the TMA tx arrive
-    mbar_init(bOdone, 1);
+    mbar_init(bOdone(0), 1);
+    mbar_init(bOdone(1), 1);
     mbar_init(bOfinal, 1);
     mbar_fence_init();
   }
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           mma_ts(tmem + C::kColO, pcol + kk * 8, bd, kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(bVempty(s));
-        tc_commit(bOdone);
+        tc_commit(bOdone(i));
         DBSP_TR(kTrMmaPV, i);
       };
       mbar_wait(bQready, 0);
@@ -384,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         issue_pv(j);
         if (j + NSB < count) {
 #ifdef DBSP_STRICT_WAR
-          mbar_wait(bOdone, j & 1);
+          mbar_wait(bOdone(j), (j >> 1) & 1);
 #endif
           issue_s(j + NSB);
         }
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           // O must be quiescent.  With one S buffer, S_j was issued after
           // PV_{j-1}, so its completion (seen above) implies PV_{j-1}'s.
           if (NSB > 1 && j > 0) {
-            mbar_wait(bOdone, (j - 1) & 1);  // completed PVs here: j-1 or j
+            mbar_wait(bOdone(j - 1), ((j - 1) >> 1) & 1);
             tc_fence_after();
           }
 #pragma unroll
