@@ -100,4 +100,14 @@ inline void sparse_attention(SpContext& ctx, const AttentionMaskSet& set, Parall
                                   q, k, v, o, set.num_q_blocks() * set.block_size(), head_dim, stream));
 }
 
+// K6: the layer's QKV projection (nn.Linear weight [3*H*d, hidden]); with
+// `scatter` non-null the Q/K/V rows go straight into the consuming ranks'
+// local buffers (the fused all-to-all(v) send of the SP call).
+inline void qkv_project(const void* x, const void* w, const void* bias, void* out, uint32_t tokens,
+                        uint32_t hidden, uint32_t heads, uint32_t head_dim, const dbsp_qkv_scatter* scatter,
+                        void* stream) {
+  const dbsp_qkv_args a{x, w, bias, out, tokens, hidden, heads, head_dim};
+  detail::check(dbsp_qkv_project(&a, scatter, stream));
+}
+
 }  // namespace dbsp

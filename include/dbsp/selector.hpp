@@ -88,4 +88,30 @@ inline Selection select(int64_t layer_id, const AttentionMaskSet& set,
   return out;
 }
 
+// select() from device-resident mask words (u64 [H][Nq][ceil(Nk/64)], the
+// BlockMask row layout): the mask integers are computed on the GPU, the
+// result equals select() on the same masks bit for bit (dbsp_select_device).
+inline Selection select_device(int64_t layer_id, const uint64_t* d_words, uint32_t heads, uint32_t q_blocks,
+                               uint32_t kv_blocks, uint32_t block_size, const MachineProfile& profile,
+                               const PlannerConfig& config, SelectorState& state, void* stream = nullptr) {
+  detail::ProfileView pv(profile);
+  Selection out;
+  out.outcome.plan.head_assignment.assign(heads, 0);
+  out.outcome.plan.q_assignment.assign(q_blocks, 0);
+  out.outcome.plan.kv_assignment.assign(kv_blocks, 0);
+  dbsp_plan c = detail::cplan(out.outcome.plan);
+  const dbsp_planner_config cfg{config.reuse_threshold, config.exchange_reward};
+  dbsp_strategy s{};
+  dbsp_plan_outcome oc{};
+  dbsp_latency lat{};
+  detail::check(dbsp_select_device(state.handle(), layer_id, d_words, heads, q_blocks, kv_blocks, block_size,
+                                   pv.get(), &cfg, &s, &c, &oc, &lat, stream));
+  out.strategy = {s.ulysses, s.ring};
+  out.outcome.head_replanned = oc.head_replanned != 0;
+  out.outcome.rho_pre = oc.rho_pre;
+  out.outcome.rho_post = oc.rho_post;
+  out.latency = detail::from_c(lat);
+  return out;
+}
+
 }  // namespace dbsp

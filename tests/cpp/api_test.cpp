@@ -92,6 +92,10 @@ int main() {
                const void*, const void*, const void*, void*, uint32_t, void*) = &dbsp::sparse_attention;
     (void)uid;
     (void)sp;
+    auto* sd = &dbsp::select_device;
+    auto* qp = &dbsp::qkv_project;
+    (void)sd;
+    (void)qp;
   }
   // c1: rho fixtures.
   {
