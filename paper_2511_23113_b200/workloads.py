@@ -58,6 +58,12 @@ WORKLOADS = {
     # C: Wan2.1-T2V-14B 480p layer (configs[2]) -- the north-star workload.
     "wan": Workload("wan2.1-14b-480p-C", 40, 128, 32768, "clustered", 0.15, 0.45, 1, 8,
                     "40 heads, d=128, 512 blocks, clustered 0.15-0.45 (mean 0.30)"),
+    # C with the other two generator families (report all
+    # three; uniform splits are already near-balanced on these).
+    "wan-random": Workload("wan2.1-14b-480p-C-random", 40, 128, 32768, "random", 0.15, 0.45, 1, 8,
+                           "as C, uniform Bernoulli masks 0.15-0.45"),
+    "wan-banded": Workload("wan2.1-14b-480p-C-banded", 40, 128, 32768, "banded", 0.15, 0.45, 1, 8,
+                           "as C, banded masks 0.15-0.45"),
     # D: HunyuanVideo 720p layer (configs[3]).
     "hunyuan": Workload("hunyuanvideo-720p-D", 24, 128, 118848, "clustered", 0.15, 0.45, 1, 8,
                         "24 heads, d=128, 1857 blocks, ~30% density"),
