@@ -210,7 +210,7 @@ def run_single(args, wl):
     out = torch.empty_like(q)
 
     t0 = time.perf_counter()
-    sched = AttentionSchedule().build(masks, kv_tokens_global=S)
+    sched = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
     build_ms = (time.perf_counter() - t0) * 1e3
     stats = sched.stats()
     sched.upload()

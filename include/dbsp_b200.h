@@ -337,7 +337,10 @@ enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER =
        DBSP_SCHED_QUAD = 8 /* 4 Q blocks per item: two 128-row tiles per CTA sharing one KV stream */,
        DBSP_SCHED_KEY128 = 16 /* with QUAD: 128-key steps (two KV blocks per tcgen05 QK^T) */,
        DBSP_SCHED_SPLIT_SOFTMAX = 32 /* with QUAD|KEY128, d=128: two softmax warps per row */,
-       DBSP_SCHED_PERSIST = 64 /* with QUAD, d=128: persistent quad kernel */ };
+       DBSP_SCHED_PERSIST = 64 /* with QUAD, d=128: persistent quad kernel */,
+       DBSP_SCHED_CTA_PAIR = 128 /* with QUAD|KEY128, d=128: CTA-pair kernel with two split-KV stages */,
+       DBSP_SCHED_AUTO_D128 = 256 /* head_dim 128: the CTA-pair quad schedule when its dense fraction is
+                                     >= 0.95 x the pair schedule's, else the pair schedule */ };
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
                         const dbsp_local_view* view, int32_t flags);

@@ -50,13 +50,14 @@ class AttentionSchedule:
 
     def build(self, masks: AttentionMaskSet, *, head_ids: Sequence[int] = None,
               q_block_ids: Sequence[int] = None, kv_block_ids: Sequence[int] = None,
-              kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None
-              ) -> "AttentionSchedule":
-        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 16 with 8: 128-key steps, 8 quad =
-        the d=128 CTA-pair kernel); default pair_q."""
+              kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None,
+              head_dim: Optional[int] = None) -> "AttentionSchedule":
+        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 8 quad, 16 with 8: 128-key
+        steps, 128 with 8|16: the d=128 CTA-pair kernel, 256 auto for d=128).  Default: pair_q, plus
+        the auto choice of the CTA-pair kernel when head_dim is 128 (DBSP_SCHED_AUTO_D128)."""
         hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
         if flags is None:
-            flags = 1 if pair_q else 0
+            flags = (1 | 256 if head_dim == 128 else 1) if pair_q else 0
         self._keep = (hid, qid, kid)
         ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32)) if a is not None else None
         view = L.LocalViewT(
@@ -202,7 +203,7 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, masks: A
         words = torch.from_numpy(masks.words.view(np.int64)).to(q.device, non_blocking=True)
         sched = AttentionSchedule().build_device(words, masks.num_kv_blocks, kv_tokens_global=Sk)
     elif sched is None:
-        sched = AttentionSchedule().build(masks, kv_tokens_global=Sk)
+        sched = AttentionSchedule().build(masks, kv_tokens_global=Sk, head_dim=q.shape[-1])
     sched.launch(q, k, v, out, lse=lse, softmax_scale=softmax_scale)
     if schedule is None:
         # keep the schedule (and its pinned staging buffer) alive until the

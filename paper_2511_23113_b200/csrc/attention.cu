@@ -21,6 +21,9 @@
 #include "attn_kernel_s32.cuh"
 #include "attn_kernel_psmem.cuh"
 #include "attn_kernel_pair.cuh"
+#include "attn_kernel_pd.cuh"
+#include "attn_kernel_pd2.cuh"
+#include "attn_kernel_pd3.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
@@ -182,6 +185,119 @@ void launch_pair(const CUtensorMap& q, const CUtensorMap& k32, const CUtensorMap
   dbsp_dev::sparse_attn_fwd_pair_kernel<<<2 * items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(
       q, k32, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_pair launch");
+}
+
+// exp2 pairs of every 8 on the FMA pipe in the CTA-pair split-KV kernels
+// (DBSP_PD_POLY=0..3; default 0: attn_kernel_pd3.cuh measured 6.12 / 6.11 /
+// 6.37 ms on Wan with 0 / 1 / 2 of 8, interleaved A/B, tests/ab_probe.py).
+int pd_poly() {
+  static const int n = [] {
+    const char* e = std::getenv("DBSP_PD_POLY");
+    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
+  }();
+  return n;
+}
+
+template <int kPoly>
+void launch_pd_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::PdCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd_kernel<kPoly>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pd)");
+  dbsp_dev::sparse_attn_fwd_pd_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd, C::kSmemBytes, stream>>>(
+      q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd launch");
+}
+
+template <int kPoly>
+void launch_pd2_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::Pd2Cfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd2_kernel<kPoly>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pd2)");
+  dbsp_dev::sparse_attn_fwd_pd2_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(
+      q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd2 launch");
+}
+
+template <int kPoly, bool kAlt>
+void launch_pd3_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::Pd3Cfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3_kernel<kPoly, kAlt>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pd3)");
+  dbsp_dev::sparse_attn_fwd_pd3_kernel<kPoly, kAlt>
+      <<<2 * items, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3 launch");
+}
+
+// DBSP_PD_ALT=1: the two stages' exp phases strictly alternate (SmDone).
+bool pd_alt() {
+  static const bool v = [] {
+    const char* e = std::getenv("DBSP_PD_ALT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+// Which CTA-pair split-KV kernel runs DBSP_SCHED_CTA_PAIR schedules
+// (DBSP_PD_VARIANT): 1 one softmax warp per row (attn_kernel_pd.cuh),
+// 2 two warps per row (attn_kernel_pd2.cuh), 3 two warps per row with P in
+// shared memory (attn_kernel_pd3.cuh, the default).
+int pd_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("DBSP_PD_VARIANT");
+    return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 3;
+  }();
+  return v;
+}
+
+void launch_pd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+               const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  if (pd_variant() == 3) {
+    const int n = pd_poly();
+    if (pd_alt()) {
+      if (n == 0) launch_pd3_n<0, true>(q, k, v, prm, items, stream);
+      else launch_pd3_n<2, true>(q, k, v, prm, items, stream);
+    } else if (n == 1) {
+      launch_pd3_n<1, false>(q, k, v, prm, items, stream);
+    } else if (n >= 2) {
+      launch_pd3_n<2, false>(q, k, v, prm, items, stream);
+    } else {
+      launch_pd3_n<0, false>(q, k, v, prm, items, stream);
+    }
+    return;
+  }
+  if (pd_variant() == 2) {
+    switch (pd_poly()) {
+      case 0: launch_pd2_n<0>(q, k, v, prm, items, stream); break;
+      case 1: launch_pd2_n<1>(q, k, v, prm, items, stream); break;
+      case 3: launch_pd2_n<3>(q, k, v, prm, items, stream); break;
+      default: launch_pd2_n<2>(q, k, v, prm, items, stream); break;
+    }
+    return;
+  }
+  switch (pd_poly()) {
+    case 0: launch_pd_n<0>(q, k, v, prm, items, stream); break;
+    case 1: launch_pd_n<1>(q, k, v, prm, items, stream); break;
+    case 3: launch_pd_n<3>(q, k, v, prm, items, stream); break;
+    default: launch_pd_n<2>(q, k, v, prm, items, stream); break;
+  }
 }
 
 template <int D>
@@ -641,7 +757,10 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       fail(kConfig, "the fused O return is not available in the opt-in pair/wide/split kernels");
     if (quad && use_pair())
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
-    else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
+    else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedCtaPair)) {
+      if (a->head_dim != 128) fail(kConfig, "the CTA-pair split-KV kernel needs head_dim 128");
+      launch_pd(tq, tk, tv, prm, n_items, stream);
+    } else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
       if (a->head_dim != 128) fail(kConfig, "the split-softmax two-stage kernel needs head_dim 128");
       launch_duo2(tq, tk, tv, prm, n_items, stream);
     } else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)

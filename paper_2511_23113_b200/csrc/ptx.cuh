@@ -181,6 +181,17 @@ __device__ __forceinline__ void setmaxnreg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
+// One lane of the (converged) warp: lets a whole warp run an MMA-issue loop
+// with warp-uniform control flow and issue each tcgen05 op from one thread,
+// without the per-instruction ELECT loop a lane-0-only branch compiles to.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- clusters / CTA pairs
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -193,9 +204,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_addr, uint32_t ra
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
   return r;
 }
+// Arrive on a (possibly remote) cluster barrier.  Default semantics
+// (.release.cta): a .release.cluster arrive compiles to MEMBAR.ALL.GPU +
+// ERRBAR + CGAERRBAR ahead of the arrive, measured at ~1600 cycles per P
+// hand-off in attn_kernel_pd.cuh.  Callers order their tcgen05 traffic with
+// tcgen05.wait + tcgen05.fence::before_thread_sync, which this arrive follows.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::

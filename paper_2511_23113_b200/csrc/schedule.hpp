@@ -58,6 +58,15 @@ constexpr uint32_t kSchedQuad = 8;       // four Q blocks per item (two-stage ke
 constexpr uint32_t kSchedKey128 = 16;    // with kSchedQuad: 128-key steps (attn_kernel_duo.cuh)
 constexpr uint32_t kSchedPersist = 64;  // with kSchedQuad, d=128: persistent quad kernel (attn_kernel_quadp.cuh)
 constexpr uint32_t kSchedSplitSoftmax = 32;  // with kSchedQuad|kSchedKey128, d=128: attn_kernel_duo2.cuh
+constexpr uint32_t kSchedCtaPair = 128;  // with kSchedQuad|kSchedKey128, d=128: attn_kernel_pd3.cuh
+// For head_dim 128: build the CTA-pair quad schedule (kSchedPairQ|kSchedQuad|
+// kSchedKey128|kSchedCtaPair) when its dense fraction is at least
+// kAutoQuadRatio of the pair schedule's, else the pair schedule.  The
+// CTA-pair kernel measured 1.04-1.08x faster per launch where four Q rows
+// share their KV blocks (Wan, HunyuanVideo, banded masks: 0.96-0.99 dense vs
+// 0.99-1.00 for pairs) and 1.23x slower on uniform random masks (0.41 vs 0.60).
+constexpr uint32_t kSchedAutoD128 = 256;
+constexpr double kAutoQuadRatio = 0.95;
 // Quad items: WorkItem{head, q0, q1, begin, count, pad_mask, q2, q3}; entries
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
 constexpr uint32_t kQuadValidShift = 26;

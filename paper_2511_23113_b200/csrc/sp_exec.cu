@@ -337,7 +337,8 @@ struct RankExec {
         v.num_kv_blocks = uint32_t(me.groups[g].size());
         v.kv_block_ids = me.groups[g].data();
         v.kv_tokens_global = tokens;
-        rc(dbsp_schedule_build(sched[g], &set, &v, 1));
+        // pair schedule, or for d=128 the CTA-pair kernel where it pays (DBSP_SCHED_AUTO_D128)
+        rc(dbsp_schedule_build(sched[g], &set, &v, d == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : 1u));
       }
     // buffers
     size_t max_g = 1;

@@ -321,7 +321,8 @@ def _cuda_attn_fn(masks: AttentionMaskSet, me: RankLayout, tokens: int, scatter=
                 scheds[g] = None
             else:
                 scheds[g] = AttentionSchedule().build(masks, head_ids=layout.heads, q_block_ids=layout.q_blocks,
-                                                      kv_block_ids=kv_blocks, kv_tokens_global=tokens)
+                                                      kv_block_ids=kv_blocks, kv_tokens_global=tokens,
+                                                      head_dim=q_loc.shape[-1])
         sc = scheds[g]
         y = layout.y
         if y == 1:
@@ -406,7 +407,7 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
             k_loc = k.index_select(0, kr).index_select(1, hs).contiguous()
             v_loc = v.index_select(0, kr).index_select(1, hs).contiguous()
             sc = AttentionSchedule().build(masks, head_ids=lay.heads, q_block_ids=lay.q_blocks,
-                                           kv_block_ids=kvb, kv_tokens_global=S)
+                                           kv_block_ids=kvb, kv_tokens_global=S, head_dim=q.shape[-1])
             sc.upload()
             if time_kernels:
                 # time on a scratch accumulator so the merge below is not disturbed
@@ -450,7 +451,7 @@ def measured_rho(times: Sequence[Sequence[float]]) -> float:
 
 
 def time_ranks_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
-                          scratch=None, reps: int = 1, flags: int = 1):
+                          scratch=None, reps: int = 1, flags: Optional[int] = None):
     """Kernel times only: every (period, rank) K4 launch of UxRy timed on this
     GPU without gathering the local buffers.  K4's cost depends on the work
     list and the buffer footprint, not on the values, so each launch runs on
@@ -486,7 +487,7 @@ def time_ranks_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelSt
             k_loc = kf[:sk * hl * d].view(sk, hl, d)
             v_loc = vf[:sk * hl * d].view(sk, hl, d)
             sc = AttentionSchedule().build(masks, head_ids=lay.heads, q_block_ids=lay.q_blocks,
-                                           kv_block_ids=kvb, kv_tokens_global=S, flags=flags)
+                                           kv_block_ids=kvb, kv_tokens_global=S, flags=flags, head_dim=d)
             sc.upload()
             best = float("inf")
             for _ in range(reps):

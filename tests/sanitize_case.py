@@ -44,8 +44,17 @@ def main():
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.2, 0.7, 1.0, 2))
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     out = torch.empty_like(q)
-    for fl in (1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64):
+    for fl in (1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128):
         AttentionSchedule().build(m, kv_tokens_global=S, flags=fl).launch(q, k, v, out)
+    # CTA-pair split-KV kernel through the ring accumulator (two KV periods)
+    o_acc = torch.empty(S, H, d, device="cuda", dtype=torch.float32)
+    l_acc = torch.empty(H, S, device="cuda", dtype=torch.float32)
+    accum_init(o_acc, l_acc)
+    for i, g in enumerate((np.arange(0, nb // 2), np.arange(nb // 2, nb))):
+        rows = torch.as_tensor((g[:, None] * 64 + np.arange(64)[None, :]).reshape(-1), device="cuda").clamp(max=S - 1)
+        kl, vl = k.index_select(0, rows).contiguous(), v.index_select(0, rows).contiguous()
+        AttentionSchedule().build(m, kv_block_ids=g, kv_tokens_global=S, flags=1 | 8 | 16 | 128).launch(
+            q, kl, vl, out, o_accum=o_acc, lse_accum=l_acc, accumulate=True, finalize=i == 1)
     torch.cuda.synchronize()
     # GPU selector, SP paths (fused O return, C++ executor), K6
     from paper_2511_23113_b200.qkv import QkvScatter, qkv_project

@@ -201,13 +201,13 @@ def test_host_streaming_equals_one_shot():
         assert torch.equal(out, ref)
 
 
-@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64])
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("H,S,Sk,pattern", [(4, 2048, None, "clustered"), (3, 1000, 2000, "random"),
                                              (5, 4096, None, "banded"), (2, 448, 4000, "random")])
 def test_two_stage_kernel(H, S, Sk, pattern, d, flags):
-    if flags & 96 and d != 128:
-        pytest.skip("the split-softmax and persistent kernels are d=128 only (d=64 falls back to quad)")
+    if flags & 224 and d != 128:
+        pytest.skip("the split-softmax, persistent and CTA-pair split-KV kernels are d=128 only")
     # quad schedule -> the two-stage kernel (two 128-row Q tiles per CTA,
     # 128-key steps); odd block counts exercise padded rows of the quad and the
     # masked second half of an odd-length step.
@@ -228,7 +228,7 @@ def test_two_stage_kernel(H, S, Sk, pattern, d, flags):
     assert np.all(np.isneginf(lse.cpu().numpy()[~fin]))
 
 
-@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64])
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128])
 def test_two_stage_ring_accumulate(flags):
     # Two KV periods through accumulate + finalize on the two-stage kernel
     # equal one pass over all KV (the K5 merge in its epilogue).

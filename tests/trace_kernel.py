@@ -23,6 +23,9 @@ def main():
     fine = args[:1] == ["--fine"]
     if fine:
         args = args[1:] + ["-DDBSP_TRACE_FINE"]
+    mma = args[:1] == ["--mma"]
+    if mma:
+        args = args[1:] + ["-DDBSP_TRACE_MMA"]
     flags = "-DDBSP_TRACE " + " ".join(args)
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    env=dict(os.environ, DBSP_NVCC_FLAGS=flags), capture_output=True)
@@ -47,6 +50,18 @@ def main():
     fn(None)
     if os.environ.get("DBSP_K4_PAIR") == "1":  # CTA-pair kernel: default-kernel event layout
         sched_flags &= ~8
+    if mma:
+        names = ["Sfree", "QK_t+2_issued", "Pfull", "Vfull", "PV_issued", "Kfull_t+2"]
+        for b in (0, 2):
+            t = tr[b].astype(np.int64)
+            n = int((t[:, 4] > 0).sum())
+            base = t[0, 2]
+            print(f"block {b}: steps={n}")
+            for j in range(min(n, 14)):
+                print("  t=%2d " % j + " ".join(f"{nm}={int(t[j, e] - base):7d}" for e, nm in enumerate(names)))
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
     if sched_flags & 8 and fine:
         fine_report(tr)
         subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
@@ -96,8 +111,11 @@ def fine_report(tr):
         for key, arr in [("ld_S", t[:, 2] - t[:, 0]), ("max", t[:, 6] - t[:, 2]), ("exp_half0", t[:, 3] - t[:, 6]),
                          ("exp_half1", t[:, 4] - t[:, 3]), ("st_wait_arrive", t[:, 1] - t[:, 4]),
                          ("total", t[:, 1] - t[:, 0]), ("P_to_PV0", t[:, 7] - t[:, 1]),
-                         ("wait_next_S", t[1:, 0] - t[:-1, 1])]:
+                         ("wait_next_S", t[1:, 0] - t[:-1, 1]), ("st_wait", t[:, 5] - t[:, 4]),
+                         ("arrive", t[:, 1] - t[:, 5])]:
             stats.setdefault(key, []).append(float(np.median(arr)))
+        if b < 4:
+            print(f"block {b}: " + json.dumps({k: v[-1] for k, v in stats.items()}))
     print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
 
 
