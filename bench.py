@@ -213,6 +213,7 @@ def run_single(args, wl):
     sched = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
     build_ms = (time.perf_counter() - t0) * 1e3
     stats = sched.stats()
+    lay = sched.layout()
     sched.upload()
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -239,7 +240,7 @@ def run_single(args, wl):
                 "traffic": ncu_traffic(wl.name), "peak_source": pk["source"],
                 "algorithmic_flops_per_launch": flops,
                 "per_unit": f"4*64*64*{d} FLOP per dense 64x64 tile x {total} dense tiles",
-                "issued_tile_frac": round(stats["dense_tiles"] / (2 * stats["tile_visits"]), 4),
+                "issued_tile_frac": round(stats["dense_tiles"] / (lay["q_blocks_per_item"] * stats["tile_visits"]), 4),
                 "kernel_ms_min": round(min(per), 4), "kernel_ms_median": round(statistics.median(per), 4)}
 
     # ---- e2e through the public API with host buffers (pinned), every step:
@@ -269,7 +270,7 @@ def run_single(args, wl):
         "config": {**wl.describe(), "parallelism": "single-gpu (U1R1)", "strategy": "U1R1",
                    "l2": "inputs larger than L2 (Q/K/V 3 x %.0f MB bf16 vs 126 MB L2)" % (q.numel() * 2 / 1e6),
                    "density": round(D.density(masks), 4), "dense_tiles": total,
-                   "schedule": {**stats, "host_build_ms": round(build_ms, 2)}},
+                   "schedule": {**stats, **lay, "host_build_ms": round(build_ms, 2)}},
         "rho_s": 1.0,
         "roofline": roofline,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d + sched_bytes,

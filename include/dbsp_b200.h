@@ -356,6 +356,10 @@ int dbsp_schedule_download(const dbsp_schedule* sched, void* items_out, uint32_t
 /* Stats of the last build: items, entries (tile visits), dense tiles. */
 int dbsp_schedule_stats(const dbsp_schedule* sched, uint64_t* items, uint64_t* tile_visits,
                         uint64_t* dense_tiles);
+/* Layout of the last build: DBSP_SCHED_* bits actually used (an AUTO_D128 build
+ * reports the schedule it chose; the 64-row Q blocks per item are 4 with
+ * DBSP_SCHED_QUAD, else 2 with DBSP_SCHED_PAIR_Q, else 1). */
+int dbsp_schedule_layout(const dbsp_schedule* sched, uint32_t* flags);
 
 /* Uploads the built schedule to the device (async on `stream`); a no-op when
  * it is already resident.  dbsp_attention_launch uploads implicitly. */

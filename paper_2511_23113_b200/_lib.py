@@ -175,6 +175,7 @@ _SIGS = {
     "dbsp_schedule_destroy": (None, [C.c_void_p]),
     "dbsp_schedule_build": (C.c_int, [C.c_void_p, P(MaskSetT), P(LocalViewT), i32]),
     "dbsp_schedule_stats": (C.c_int, [C.c_void_p, P(u64), P(u64), P(u64)]),
+    "dbsp_schedule_layout": (C.c_int, [C.c_void_p, P(u32)]),
     "dbsp_schedule_build_device": (C.c_int, [C.c_void_p, C.c_void_p, u32, u32, u32, P(LocalViewT), i32,
                                              C.c_void_p]),
     "dbsp_schedule_download": (C.c_int, [C.c_void_p, C.c_void_p, P(u32), u64]),

@@ -101,6 +101,16 @@ class AttentionSchedule:
         check(L.lib().dbsp_schedule_stats(self._h, C.byref(items), C.byref(visits), C.byref(dense)))
         return {"items": items.value, "tile_visits": visits.value, "dense_tiles": dense.value}
 
+    def layout(self) -> dict:
+        """Schedule flags actually built (an auto build reports its choice) and the 64-row Q
+        blocks each work item covers (its M per tile visit)."""
+        f = C.c_uint32()
+        check(L.lib().dbsp_schedule_layout(self._h, C.byref(f)))
+        rows = 4 if f.value & 8 else 2 if f.value & 1 else 1
+        return {"flags": f.value, "q_blocks_per_item": rows,
+                "kernel": "cta_pair_split_kv" if (f.value & 8 and f.value & 128) else
+                          "two_stage" if f.value & 8 else "pair_items"}
+
     def upload(self, stream: Optional[torch.cuda.Stream] = None) -> int:
         """Make the schedule device-resident (no-op if already); returns bytes moved."""
         s = stream if stream is not None else torch.cuda.current_stream()

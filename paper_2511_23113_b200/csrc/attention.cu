@@ -666,6 +666,13 @@ int dbsp_schedule_stats(const dbsp_schedule* s, uint64_t* items, uint64_t* visit
   });
 }
 
+int dbsp_schedule_layout(const dbsp_schedule* s, uint32_t* flags) {
+  return guard([&] {
+    if (!s || !flags) fail(kContract, "null argument");
+    *flags = s->on_device ? uint32_t(kSchedPairQ) : s->host.flags;  // K2 builds pair schedules
+  });
+}
+
 int dbsp_schedule_download(const dbsp_schedule* s, void* items_out, uint32_t* entries_out,
                            uint64_t max_entries) {
   return guard([&] {

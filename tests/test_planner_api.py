@@ -415,4 +415,5 @@ def test_auto_d128_schedule_choice():
         fixed = AttentionSchedule().build(m, flags=1 | 8 | 16 | 128 if per_item == 4 else 1).stats()
         assert auto == fixed, pattern
         assert auto["items"] == H * (nb // per_item), pattern
+        assert AttentionSchedule().build(m, head_dim=128).layout()["q_blocks_per_item"] == per_item
         assert AttentionSchedule().build(m, head_dim=64).stats()["items"] == H * (nb // 2)
