@@ -38,6 +38,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 }
 // Blocks until the phase with the given parity has completed.  With
 // DBSP_WATCHDOG a wait that never completes traps (an error, not a hang).
+// Non-blocking probe of a phase (mbarrier.test_wait): for issuers that poll
+// several barriers and act on whichever completes first.
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifdef DBSP_WATCHDOG
   uint32_t spins = 0;
