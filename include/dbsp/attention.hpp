@@ -32,22 +32,23 @@ class AttentionSchedule {
   AttentionSchedule(const AttentionSchedule&) = delete;
   AttentionSchedule& operator=(const AttentionSchedule&) = delete;
 
-  // Whole-problem schedule (identity local view).
-  void build(const AttentionMaskSet& set, uint32_t kv_tokens) {
+  // Whole-problem schedule (identity local view).  head_dim 128 lets the builder
+  // pick the CTA-pair kernel where it pays (DBSP_SCHED_AUTO_D128).
+  void build(const AttentionMaskSet& set, uint32_t kv_tokens, uint32_t head_dim = 0) {
     detail::MaskView v(set);
     dbsp_local_view lv{set.num_heads(), nullptr, set.num_q_blocks(), nullptr,
                        set.num_kv_blocks(), nullptr, kv_tokens};
-    detail::check(dbsp_schedule_build(h_, v.get(), &lv, 1));
+    detail::check(dbsp_schedule_build(h_, v.get(), &lv, flags_for(head_dim)));
   }
   // One rank's share: local head / Q-block / KV-block ids in buffer order.
   void build(const AttentionMaskSet& set, const std::vector<uint32_t>& heads,
              const std::vector<uint32_t>& q_blocks, const std::vector<uint32_t>& kv_blocks,
-             uint32_t kv_tokens_global) {
+             uint32_t kv_tokens_global, uint32_t head_dim = 0) {
     detail::MaskView v(set);
     dbsp_local_view lv{uint32_t(heads.size()), heads.data(), uint32_t(q_blocks.size()),
                        q_blocks.data(), uint32_t(kv_blocks.size()), kv_blocks.data(),
                        kv_tokens_global};
-    detail::check(dbsp_schedule_build(h_, v.get(), &lv, 1));
+    detail::check(dbsp_schedule_build(h_, v.get(), &lv, flags_for(head_dim)));
   }
   void launch(const AttentionArgs& a, void* stream) {
     const dbsp_attn_args c{a.q, a.k, a.v, a.o, a.lse, nullptr, nullptr, a.q_tokens, a.kv_tokens,
@@ -57,6 +58,9 @@ class AttentionSchedule {
   dbsp_schedule* handle() const { return h_; }
 
  private:
+  static int32_t flags_for(uint32_t head_dim) {
+    return head_dim == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : DBSP_SCHED_PAIR_Q;
+  }
   dbsp_schedule* h_ = nullptr;
 };
 

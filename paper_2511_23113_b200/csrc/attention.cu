@@ -829,7 +829,9 @@ int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, 
     v.num_kv_blocks = set->num_kv_blocks;
     v.kv_tokens_global = args ? args->kv_tokens : 0;
   }
-  const int rc = dbsp_schedule_build(sched, set, &v, 1);
+  // pair schedule; for d=128 the CTA-pair kernel where its quads stay dense
+  const int32_t flags = (args && args->head_dim == 128) ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : 1;
+  const int rc = dbsp_schedule_build(sched, set, &v, flags);
   if (rc) return rc;
   return dbsp_attention_launch(sched, args, stream);
 }
