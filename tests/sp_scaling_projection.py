@@ -34,7 +34,7 @@ def main():
         H, S, d = wl.heads, wl.tokens, wl.head_dim
         g = torch.Generator(device="cuda").manual_seed(1234)
         q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
-        sc = AttentionSchedule().build(masks, kv_tokens_global=S)
+        sc = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
         sc.upload()
         o = torch.empty_like(q)
         for _ in range(2):
