@@ -242,6 +242,15 @@ def run_single(args, wl):
                 "per_unit": f"4*64*64*{d} FLOP per dense 64x64 tile x {total} dense tiles",
                 "issued_tile_frac": round(stats["dense_tiles"] / (lay["q_blocks_per_item"] * stats["tile_visits"]), 4),
                 "kernel_ms_min": round(min(per), 4), "kernel_ms_median": round(statistics.median(per), 4)}
+    # Second ceiling: the softmax's exp2 on the MUFU pipe, 16 per clock per SM on B200
+    # (tests/ex2h_bench.cu), at the clock measured inside the kernel.  At d=64 a 64x64
+    # tile's 4096 exps take twice its tensor time, so d=64 layers are exp-bound.
+    exps = total * 64 * 64
+    mufu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * (kernel_mhz or 1965.0) * 1e6
+    roofline["softmax_exp2"] = {"per_launch": exps, "achieved_per_s": round(exps / (ms * 1e-3), 1),
+                                "peak_per_s": round(mufu_peak, 1), "frac": round(exps / (ms * 1e-3) / mufu_peak, 4),
+                                "peak_basis": "16 ex2/clk/SM x SMs x in-kernel SM clock; d=64 runs 2 of 8 exp pairs "
+                                              "on the FMA pipe, so frac may exceed 1 there"}
 
     # ---- e2e through the public API with host buffers (pinned), every step:
     # H2D of Q/K/V, host schedule build from the masks (C++), upload, kernel, D2H of O.
