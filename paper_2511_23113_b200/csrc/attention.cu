@@ -24,6 +24,7 @@
 #include "attn_kernel_pd.cuh"
 #include "attn_kernel_pd2.cuh"
 #include "attn_kernel_pd3.cuh"
+#include "attn_kernel_pd4.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
@@ -255,6 +256,22 @@ bool pd_alt() {
   return v;
 }
 
+template <int kPoly>
+void launch_pd4_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::Pd4Cfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd4_kernel<kPoly>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pd4)");
+  dbsp_dev::sparse_attn_fwd_pd4_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd4, C::kSmemBytes, stream>>>(
+      q, k, v, prm);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd4 launch");
+}
+
 // Which CTA-pair split-KV kernel runs DBSP_SCHED_CTA_PAIR schedules
 // (DBSP_PD_VARIANT): 1 one softmax warp per row (attn_kernel_pd.cuh),
 // 2 two warps per row (attn_kernel_pd2.cuh), 3 two warps per row with P in
@@ -262,13 +279,20 @@ bool pd_alt() {
 int pd_variant() {
   static const int v = [] {
     const char* e = std::getenv("DBSP_PD_VARIANT");
-    return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 3;
+    return (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 3;
   }();
   return v;
 }
 
 void launch_pd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  if (pd_variant() == 4) {
+    const int n = pd_poly();
+    if (n == 0) launch_pd4_n<0>(q, k, v, prm, items, stream);
+    else if (n == 1) launch_pd4_n<1>(q, k, v, prm, items, stream);
+    else launch_pd4_n<2>(q, k, v, prm, items, stream);
+    return;
+  }
   if (pd_variant() == 3) {
     const int n = pd_poly();
     if (pd_alt()) {
