@@ -444,3 +444,26 @@ def test_empty_heads_rows_and_quads_every_kernel(flags):
     fin = np.isfinite(ref_lse)
     assert np.array_equal(fin, np.isfinite(lse.cpu().numpy()))
     assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+
+
+@pytest.mark.parametrize("flags", [1, 1 | 8 | 16 | 128])
+def test_fused_scatter_every_d128_kernel(flags):
+    # The fused O return through the one-CTA and the CTA-pair kernels: rows of
+    # local Q block b go to "rank" b % 2 at home block b // 2, local head h to
+    # home head H-1-h -- the same rows as the plain launch, permuted.
+    from paper_2511_23113_b200.attention import OutScatter
+    H, S, d = 6, 2048, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.2, 0.5, 1.0, 41))
+    q, k, v = (t.cuda() for t in make_qkv(S, H, d, 42))
+    sc = AttentionSchedule().build(masks, kv_tokens_global=S, flags=flags)
+    ref = torch.empty_like(q)
+    sc.launch(q, k, v, ref)
+    homes = [torch.zeros(S // 2, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+    qmap = np.array([[b % 2, (b // 2) * 64, 64] for b in range(nb)])
+    scat = OutScatter([t.data_ptr() for t in homes], qmap, list(range(H - 1, -1, -1)), H, "cuda")
+    sc.launch(q, k, v, None, scatter=scat)
+    torch.cuda.synchronize()
+    for b in range(nb):
+        got = homes[b % 2][(b // 2) * 64:(b // 2 + 1) * 64].flip(1)
+        assert torch.equal(got, ref[b * 64:(b + 1) * 64]), f"flags {flags} block {b}"
