@@ -339,17 +339,18 @@ void launch_duo(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo launch");
 }
 
+template <int D>
 void launch_duo2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::Duo2Cfg;
+  using C = dbsp_dev::Duo2Cfg<D>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo2_kernel,
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo2_kernel<D>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute(duo2)");
-  dbsp_dev::sparse_attn_fwd_duo2_kernel<<<items, dbsp_dev::kThreadsDuo2, C::kSmemBytes, stream>>>(q, k, v, prm);
+  dbsp_dev::sparse_attn_fwd_duo2_kernel<D><<<items, dbsp_dev::kThreadsDuo2, C::kSmemBytes, stream>>>(q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo2 launch");
 }
 
@@ -792,8 +793,10 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       if (a->head_dim != 128) fail(kConfig, "the CTA-pair split-KV kernel needs head_dim 128");
       launch_pd(tq, tk, tv, prm, n_items, stream);
     } else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
-      if (a->head_dim != 128) fail(kConfig, "the split-softmax two-stage kernel needs head_dim 128");
-      launch_duo2(tq, tk, tv, prm, n_items, stream);
+      if (a->head_dim == 128)
+        launch_duo2<128>(tq, tk, tv, prm, n_items, stream);
+      else
+        launch_duo2<64>(tq, tk, tv, prm, n_items, stream);
     } else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
       launch_duo<128>(tq, tk, tv, prm, n_items, stream);
     else if (quad && (h.flags & kSchedKey128))

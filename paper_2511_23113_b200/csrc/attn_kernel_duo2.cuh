@@ -36,13 +36,16 @@ constexpr int kThreadsDuo2 = 640;
 #endif
 constexpr int kDuo2PolyPairs = DBSP_DUO2_POLY;  // exp2 pairs of every 8 on the FMA pipe
 
+template <int kD>
 struct Duo2Cfg {
-  static constexpr int D = 128;
+  static constexpr int D = kD;
+  static constexpr int kChunks = D / 64;          // 128-byte swizzle atoms along d
+  static constexpr uint32_t kOHalf = D / 2;       // O columns per key-half warp
   static constexpr uint32_t kQStageBytes = 128u * D * 2u;
   static constexpr uint32_t kQBytes = 2u * kQStageBytes;
   static constexpr uint32_t kChunkBytes = 128u * 128u;  // 128 rows x 128 B
   static constexpr uint32_t kStepBytes = 128u * D * 2u;  // one 128-key K or V step
-  static constexpr uint32_t kColS = 0, kColO = 256;
+  static constexpr uint32_t kColS = 0, kColO = 256;  // O_s at kColO + D s
   static constexpr int kStages = 2;
   static constexpr int kNumBars = 4 * kStages + 10;
   static constexpr uint32_t kXBytes = 2u * 2u * 2u * 128u * 4u;  // [parity][stage][half][row] max
@@ -51,11 +54,12 @@ struct Duo2Cfg {
       kQBytes + 2u * kStages * kStepBytes + kXBytes + kLBytes + 1024 + 8 * kNumBars + 16;
 };
 
+template <int kD>
 __global__ void __launch_bounds__(kThreadsDuo2, 1)
     sparse_attn_fwd_duo2_kernel(const __grid_constant__ CUtensorMap tmQ,
                                 const __grid_constant__ CUtensorMap tmK,
                                 const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using C = Duo2Cfg;
+  using C = Duo2Cfg<kD>;
   constexpr int D = C::D;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
         for (int st = 0; st < 2; ++st) {
           mbar_expect_tx(bQready(st), C::kQStageBytes);
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < C::kChunks; ++c) {
             const uint32_t dst = sQ + st * C::kQStageBytes + c * C::kChunkBytes;
             tma_load_3d(dst, &tmQ, c * 64, head, int(qblk(2 * st)) * 64, bQready(st), pol_q);
             tma_load_3d(dst + 8192, &tmQ, c * 64, head, int(qblk(2 * st + 1)) * 64, bQready(st), pol_q);
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
           const int kv1 = 2 * t + 1 < count ? int(__ldg(ent + 2 * t + 1) & dbsp_core::kEntryKvMask) : kv0;
           mbar_expect_tx(full, C::kStepBytes);
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < C::kChunks; ++c) {
             tma_load_3d(dst + c * C::kChunkBytes, tm, c * 64, head, kv0 * 64, full, pol_kv);
             tma_load_3d(dst + c * C::kChunkBytes + 8192, tm, c * 64, head, kv1 * 64, full, pol_kv);
           }
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
         constexpr uint32_t kIdescQK = idesc_bf16(128, 128, false, false);
         constexpr uint32_t kIdescPV = idesc_bf16(128, D, false, true);
         const uint32_t scol = tmem + C::kColS + 128u * st;
-        const uint32_t ocol = tmem + C::kColO + 128u * st;
+        const uint32_t ocol = tmem + C::kColO + uint32_t(D) * st;
         auto issue_s = [&](uint32_t t) {
           const int s = int(t % NS);
           mbar_wait(bKfull(s), (t / NS) & 1);
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
     const bool padded = (it.single >> bi) & 1u;
     const uint32_t lane_off = uint32_t(lg * 32) << 16;
     const uint32_t scol = tmem + lane_off + C::kColS + 128u * st + 64u * hf;
-    const uint32_t ocol = tmem + lane_off + C::kColO + 128u * st + 64u * hf;
+    const uint32_t ocol = tmem + lane_off + C::kColO + uint32_t(D) * st + C::kOHalf * hf;
     const uint32_t bar_id = 1u + 4u * st + lg;  // the two warps (hf 0/1) of these rows
     const uint32_t dense_bit = 1u << (22 + bi);
     const float sl2 = p.scale_log2;
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
       if (__any_sync(0xffffffffu, need_o)) {
         // O_s is quiescent: S_s(t) (complete) was issued after PV_s(t-1).
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < int(C::kOHalf / 32); ++c) {
           uint32_t o[32];
           tmem_ld32(ocol + c * 32, o);
           tmem_ld_wait();
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
     const bool live = !padded && token < p.q_tokens;
     const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
     const float lse_new = lt > 0.f ? (m + log2f(lt)) * 0.6931471805599453f : -INFINITY;
-    const size_t orow = (size_t(token) * p.heads + it.head) * D + 64u * hf;
+    const size_t orow = (size_t(token) * p.heads + it.head) * D + C::kOHalf * hf;
     const size_t lidx = size_t(it.head) * p.q_tokens + token;
     float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
     const bool acc = (p.mode & kModeAccumulate) != 0;
@@ -376,10 +380,10 @@ __global__ void __launch_bounds__(kThreadsDuo2, 1)
       named_bar_sync(bar_id, 64);  // both halves read lse_acc before half 0 rewrites it
     }
     bool live_out = live;
-    __nv_bfloat16* const optr = out_row_ptr<D>(p, token, it.head, live_out) + 64u * hf;
+    __nv_bfloat16* const optr = out_row_ptr<D>(p, token, it.head, live_out) + C::kOHalf * hf;
     const bool write_bf16 = !acc || (p.mode & kModeFinalize);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < int(C::kOHalf / 32); ++c) {
       uint32_t o[32];
       if (count > 0) {
         tmem_ld32(ocol + c * 32, o);
