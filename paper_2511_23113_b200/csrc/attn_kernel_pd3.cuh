@@ -401,8 +401,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
           tmem_st32(ocol + c * 32, o);
         }
+        tmem_st_wait();  // the only TMEM stores of the step
       }
-      tmem_st_wait();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic writes) -> tensor core
       tc_fence_before();
       __syncwarp();
