@@ -94,6 +94,7 @@ int main() {
   dbsp::sparse_attention(m2, args, nullptr);
   cudaMemcpy(ho.data(), dout, n * 2, cudaMemcpyDeviceToHost);
   // CPU reference on sampled rows: softmax over the dense tiles of the row's Q block
+  auto sampled_error = [&](const std::vector<__nv_bfloat16>& ho) {
   double max_err = 0.0;
   const float scale = 1.0f / std::sqrt(float(d));
   for (uint32_t h = 0; h < H; ++h)
@@ -119,8 +120,31 @@ int main() {
         max_err = std::max(max_err, std::fabs(o - double(__bfloat162float(ho[(size_t(t) * H + h) * d + c]))));
       }
     }
+  return max_err;
+  };
+  const double max_err = sampled_error(ho);
   std::printf("attention max-abs error on sampled rows: %.3e\n", max_err);
   EXPECT(max_err <= 2e-2, "dbsp::sparse_attention matches the CPU reference within 2e-2");
+
+  // ---- the CTA-pair kernel (cta_group::2, attn_kernel_pd3.cuh) through the C ABI
+  {
+    dbsp::detail::MaskView mv(m2);
+    dbsp_schedule* sch = nullptr;
+    EXPECT(dbsp_schedule_create(&sch) == 0, "schedule create");
+    dbsp_local_view lv{H, nullptr, nb, nullptr, nb, nullptr, S};
+    const int32_t fl = DBSP_SCHED_PAIR_Q | DBSP_SCHED_QUAD | DBSP_SCHED_KEY128 | DBSP_SCHED_CTA_PAIR;
+    EXPECT(dbsp_schedule_build(sch, mv.get(), &lv, fl) == 0, "CTA-pair schedule build");
+    uint32_t got_flags = 0;
+    EXPECT(dbsp_schedule_layout(sch, &got_flags) == 0 && got_flags == uint32_t(fl), "schedule layout reports the CTA-pair build");
+    cudaMemset(dout, 0, n * 2);
+    const dbsp_attn_args ca{dq, dk, dv, dout, nullptr, nullptr, nullptr, S, S, H, d, 0.f, 0, 0};
+    EXPECT(dbsp_attention_launch(sch, &ca, nullptr) == 0, "CTA-pair launch");
+    cudaMemcpy(ho.data(), dout, n * 2, cudaMemcpyDeviceToHost);
+    const double e2 = sampled_error(ho);
+    std::printf("CTA-pair kernel max-abs error on sampled rows: %.3e\n", e2);
+    EXPECT(e2 <= 2e-2, "the CTA-pair kernel matches the CPU reference within 2e-2");
+    dbsp_schedule_destroy(sch);
+  }
   cudaFree(dq);
   cudaFree(dk);
   cudaFree(dv);

@@ -30,7 +30,8 @@ def test_cpp_api_compiles_links_and_passes(tmp_path):
 @pytest.mark.skipif(shutil.which("g++") is None, reason="needs g++")
 def test_cpp_gpu_faces(tmp_path):
     # tests/cpp/gpu_api_test.cpp: dbsp::select_device vs dbsp::select, and
-    # dbsp::sparse_attention vs a CPU reference, from plain C++.
+    # dbsp::sparse_attention and the CTA-pair kernel (C ABI, DBSP_SCHED_CTA_PAIR) vs a
+    # CPU reference, from plain C++.
     lib_dir = ROOT / "paper_2511_23113_b200"
     exe = tmp_path / "gpu_api_test"
     prof = ROOT / "paper_2511_23113_b200" / "profiles" / "b200_wan_measured.json"
