@@ -25,6 +25,7 @@
 #include "attn_kernel_pd2.cuh"
 #include "attn_kernel_pd3.cuh"
 #include "attn_kernel_pd4.cuh"
+#include "attn_kernel_pd3p.cuh"
 #include "attn_kernel_split.cuh"
 #include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
@@ -270,6 +271,25 @@ void launch_pd4_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap&
   dbsp_dev::sparse_attn_fwd_pd4_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd4, C::kSmemBytes, stream>>>(
       q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd4 launch");
+}
+
+void launch_pd3p(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+  using C = dbsp_dev::Pd3pCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int sms = 148;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3p_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  });
+  cuda_check(attr_err, "cudaFuncSetAttribute(pd3p)");
+  const uint32_t clusters = std::min<uint32_t>(items, uint32_t(sms / 2));  // one persistent CTA pair per TPC
+  dbsp_dev::sparse_attn_fwd_pd3p_kernel<<<2 * clusters, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(
+      q, k, v, prm, items);
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3p launch");
 }
 
 // Which CTA-pair split-KV kernel runs DBSP_SCHED_CTA_PAIR schedules
@@ -791,7 +811,15 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
     else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedCtaPair)) {
       if (a->head_dim != 128) fail(kConfig, "the CTA-pair split-KV kernel needs head_dim 128");
-      launch_pd(tq, tk, tv, prm, n_items, stream);
+      if (h.flags & kSchedPersist) {
+        if (!sched->item_counter)
+          cuda_check(cudaMalloc(&sched->item_counter, sizeof(unsigned int)), "cudaMalloc item counter");
+        cuda_check(cudaMemsetAsync(sched->item_counter, 0, sizeof(unsigned int), stream), "memset item counter");
+        prm.item_counter = sched->item_counter;
+        launch_pd3p(tq, tk, tv, prm, n_items, stream);
+      } else {
+        launch_pd(tq, tk, tv, prm, n_items, stream);
+      }
     } else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
       if (a->head_dim == 128)
         launch_duo2<128>(tq, tk, tv, prm, n_items, stream);

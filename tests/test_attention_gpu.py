@@ -201,7 +201,8 @@ def test_host_streaming_equals_one_shot():
         assert torch.equal(out, ref)
 
 
-@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128])
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128,
+                                   1 | 8 | 16 | 64 | 128])
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("H,S,Sk,pattern", [(4, 2048, None, "clustered"), (3, 1000, 2000, "random"),
                                              (5, 4096, None, "banded"), (2, 448, 4000, "random")])
@@ -228,7 +229,8 @@ def test_two_stage_kernel(H, S, Sk, pattern, d, flags):
     assert np.all(np.isneginf(lse.cpu().numpy()[~fin]))
 
 
-@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128])
+@pytest.mark.parametrize("flags", [1 | 8, 1 | 8 | 16, 1 | 8 | 16 | 32, 1 | 8 | 64, 1 | 8 | 16 | 128,
+                                   1 | 8 | 16 | 64 | 128])
 def test_two_stage_ring_accumulate(flags):
     # Two KV periods through accumulate + finalize on the two-stage kernel
     # equal one pass over all KV (the K5 merge in its epilogue).
@@ -446,7 +448,7 @@ def test_empty_heads_rows_and_quads_every_kernel(flags):
     assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
 
 
-@pytest.mark.parametrize("flags", [1, 1 | 8 | 16 | 128])
+@pytest.mark.parametrize("flags", [1, 1 | 8 | 16 | 128, 1 | 8 | 16 | 64 | 128])
 def test_fused_scatter_every_d128_kernel(flags):
     # The fused O return through the one-CTA and the CTA-pair kernels: rows of
     # local Q block b go to "rank" b % 2 at home block b // 2, local head h to
