@@ -10,7 +10,10 @@
 // leader).  Barrier phases run on cumulative counters: K/V ring steps, per-
 // stage S/P uses, and non-empty items (Q full, Qfree after an item's last
 // QK^T, Ofinal after its last PV, Odrained after both CTAs' epilogues read O).
-// Warp roles, TMEM and the epilogue are those of attn_kernel_pd3.cuh.
+// Warp roles, TMEM and the epilogue are those of attn_kernel_pd3.cuh; setmaxnreg
+// 112/32 (at 104 the item-loop state spills the softmax: 9.4 ms on Wan).
+// Status: parity-green, opt-in (schedule flags 217); measured 1-2% slower than
+// the non-persistent kernel (Wan 6.27 vs 6.19 ms, HunyuanVideo 46.1 vs 45.0).
 // Mask semantics follow the reference BlockMask (mask.hpp:18-20).
 #pragma once
 
