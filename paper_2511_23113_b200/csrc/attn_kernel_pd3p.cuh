@@ -12,8 +12,9 @@
 // QK^T, Ofinal after its last PV, Odrained after both CTAs' epilogues read O).
 // Warp roles, TMEM and the epilogue are those of attn_kernel_pd3.cuh; setmaxnreg
 // 112/32 (at 104 the item-loop state spills the softmax: 9.4 ms on Wan).
-// Status: parity-green, opt-in (schedule flags 217); measured 1-2% slower than
-// the non-persistent kernel (Wan 6.27 vs 6.19 ms, HunyuanVideo 46.1 vs 45.0).
+// Status: parity-green, opt-in (schedule flags 217).  With the softmax warps'
+// item state in shared memory: Wan 6.19 vs 6.26 ms for the non-persistent
+// kernel (short items gain), HunyuanVideo 46.2 vs 45.3 (long items lose).
 // Mask semantics follow the reference BlockMask (mask.hpp:18-20).
 #pragma once
 
@@ -36,7 +37,8 @@ struct Pd3pCfg {
   static constexpr uint32_t kXBytes = 2u * 2u * 2u * 128u * 4u;  // [parity][stage][half][row] partial max
   static constexpr uint32_t kMlBytes = 2u * 2u * 2u * 128u * 8u;  // [item parity][stage][half][row] (m, l)
   static constexpr uint32_t kSmemBytes =
-      kQBytes + kStages * (kKStep + kVStep) + 2 * kPBytes + kXBytes + kMlBytes + 1024 + 8 * kNumBars + 16 + 8 * kItemSlots;
+      kQBytes + kStages * (kKStep + kVStep) + 2 * kPBytes + kXBytes + kMlBytes + 1024 + 8 * kNumBars + 16 + 8 * kItemSlots +
+      16 * 16;  // per softmax warp: {item count, item id, non-empty items}
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
@@ -77,6 +79,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
   auto bItemEmpty = [&](int k) { return sBar + 8u * (4 * NS + 14 + C::kItemSlots + k); };  // leader
   const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
   const uint32_t sRing = sTmemSlot + 16;  // kItemSlots x {item id, sequence}
+  const uint32_t sWst = sRing + 8u * C::kItemSlots;  // softmax warps' item-loop state
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -329,10 +332,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
     const uint32_t sfree_remote_base = rank ? leader(bSfree(0)) : 0u;
     uint8_t* const prow0 = gbase + (sP - base) + hf * 16384 + row * 128;  // + st * kPBytes
     const float sl2 = p.scale_log2;
-    uint32_t gu = 0, nz = 0;  // this stage's cumulative S/P uses, non-empty items
-    for (uint32_t k = 0;; ++k) {
-    const uint32_t id = take_item(k);
+    // Item-loop state other than gu lives in shared memory (wst: item count k,
+    // item id, non-empty items nz) so that it holds no registers across the step
+    // loop; at 112 registers the softmax has none to spare.
+    volatile uint32_t* const wst = reinterpret_cast<volatile uint32_t*>(gbase + (sWst - base)) + 4 * warp;
+    if (lane == 0) {
+      wst[0] = 0;
+      wst[1] = 0;
+      wst[2] = 0;
+    }
+    __syncwarp();
+    uint32_t gu = 0;  // this stage's cumulative S/P uses
+    for (;;) {
+    const uint32_t id = take_item(wst[0]);
     if (id >= n_items) break;
+    if (lane == 0) wst[1] = id;
     // only what the step loop needs stays live; the epilogue re-reads the item
     const uint32_t count = __ldg(&p.items[id].count);
     const uint32_t nsteps = (count + 1) / 2;
@@ -490,12 +504,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
 
     // ------------------------------------------------------------ epilogue: 32 columns per thread
     if (count > 0) {
-      mbar_wait(bOfinal, nz & 1);
+      mbar_wait(bOfinal, wst[2] & 1);
       tc_fence_after();
     }
-    const WorkItem it = p.items[id];
+    __syncwarp();
+    const WorkItem it = p.items[wst[1]];
     const uint32_t myq[2] = {rank ? it.pad0 : it.qa, rank ? it.pad1 : it.qb};  // quad rows 2r, 2r+1
-    float2* const mlk = mlbuf + (k & 1u) * 512;  // by item parity: a partner may still read the last one
+    float2* const mlk = mlbuf + (wst[0] & 1u) * 512;  // by item parity: a partner may still read the last one
     mlk[(st * 2 + hf) * 128 + row] = make_float2(m, l);
     const uint32_t ebar = 9u + lg;  // the four warps (stage x half) of these rows
     named_bar_sync(ebar, 128);
@@ -601,8 +616,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
         else
           mbar_arrive_cluster(leader(bOdrained));
       }
-      ++nz;
     }
+    __syncwarp();
+    if (lane == 0) {
+      wst[0] = wst[0] + 1;
+      if (count > 0) wst[2] = wst[2] + 1;
+    }
+    __syncwarp();
     gu += (nsteps + 1 - uint32_t(st)) / 2;
     }  // item loop
     if (p.out_peers) __threadfence_system();
