@@ -28,7 +28,7 @@ def main():
     samples = []
     for dens in (0.1, 0.2, 0.3, 0.45, 0.6, 0.8, 1.0):
         m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, wl.pattern, dens, dens, 1.0, 3))
-        sc = AttentionSchedule().build(m, kv_tokens_global=S)
+        sc = AttentionSchedule().build(m, kv_tokens_global=S, head_dim=d)
         sc.upload()
         for _ in range(3):
             sc.launch(q, k, v, out)
