@@ -334,13 +334,13 @@ void dbsp_schedule_destroy(dbsp_schedule* sched);
  * heads, HEAD_ORDER within each head (K/V of concurrently running CTAs stays
  * L2-resident); with neither, small local problems get GLOBAL_LPT. */
 enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4,
-       DBSP_SCHED_QUAD = 8 /* 4 Q blocks per item: two 128-row tiles per CTA sharing one KV stream */,
-       DBSP_SCHED_KEY128 = 16 /* with QUAD: 128-key steps (two KV blocks per tcgen05 QK^T) */,
-       DBSP_SCHED_SPLIT_SOFTMAX = 32 /* with QUAD|KEY128, d=128: two softmax warps per row */,
-       DBSP_SCHED_PERSIST = 64 /* with QUAD, d=128: persistent quad kernel */,
-       DBSP_SCHED_CTA_PAIR = 128 /* with QUAD|KEY128, d=128: CTA-pair kernel with two split-KV stages */,
+       DBSP_SCHED_QUAD = 8 /* layout bit: 4 Q blocks per item (set by CTA_PAIR) */,
+       DBSP_SCHED_KEY128 = 16 /* layout bit: 128-key steps (set by CTA_PAIR) */,
+       DBSP_SCHED_CTA_PAIR = 128 /* head_dim 128: quad items for the CTA-pair kernel (cta_group::2, two
+                                    split-KV stages); implies PAIR_Q | QUAD | KEY128 */,
        DBSP_SCHED_AUTO_D128 = 256 /* head_dim 128: the CTA-pair quad schedule when its dense fraction is
                                      >= 0.95 x the pair schedule's, else the pair schedule */ };
+/* QUAD or KEY128 without CTA_PAIR, and any other bit, are DBSP_CONFIG_ERROR. */
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
                         const dbsp_local_view* view, int32_t flags);

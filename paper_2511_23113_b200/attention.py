@@ -52,8 +52,8 @@ class AttentionSchedule:
               q_block_ids: Sequence[int] = None, kv_block_ids: Sequence[int] = None,
               kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None,
               head_dim: Optional[int] = None) -> "AttentionSchedule":
-        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 8 quad, 16 with 8: 128-key
-        steps, 128 with 8|16: the d=128 CTA-pair kernel, 256 auto for d=128).  Default: pair_q, plus
+        """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 128 the d=128 CTA-pair
+        kernel's quad items (adds the layout bits 8|16), 256 auto choice for d=128).  Default: pair_q, plus
         the auto choice of the CTA-pair kernel when head_dim is 128 (DBSP_SCHED_AUTO_D128)."""
         hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
         if flags is None:
@@ -69,10 +69,16 @@ class AttentionSchedule:
         return self
 
     def build_device(self, words: torch.Tensor, num_kv_blocks: int, *, head_ids=None, q_block_ids=None,
-                     kv_block_ids=None, kv_tokens_global: int = 0, flags: int = 1,
+                     kv_block_ids=None, kv_tokens_global: int = 0, flags: Optional[int] = None,
+                     head_dim: Optional[int] = None,
                      stream: Optional[torch.cuda.Stream] = None) -> "AttentionSchedule":
         """K2: build the work list on the GPU from device mask words (int64
-        [H, Nq, ceil(Nk/64)], the BlockMask row layout)."""
+        [H, Nq, ceil(Nk/64)], the BlockMask row layout).  flags as in build();
+        default: pair items, and for head_dim 128 the auto choice, made on the
+        device (both layouts are built, both kernels launched, the kernel not
+        chosen returns at once)."""
+        if flags is None:
+            flags = 1 | 256 if head_dim == 128 else 1
         if not words.is_cuda or words.dtype != torch.int64 or words.dim() != 3 or not words.is_contiguous():
             raise ContractError("device mask words must be a contiguous CUDA int64 [H, Nq, words] tensor")
         H, nq, _ = words.shape
@@ -108,8 +114,7 @@ class AttentionSchedule:
         check(L.lib().dbsp_schedule_layout(self._h, C.byref(f)))
         rows = 4 if f.value & 8 else 2 if f.value & 1 else 1
         return {"flags": f.value, "q_blocks_per_item": rows,
-                "kernel": "cta_pair_split_kv" if (f.value & 8 and f.value & 128) else
-                          "two_stage" if f.value & 8 else "pair_items"}
+                "kernel": "cta_pair_split_kv" if f.value & 128 else "pair_items"}
 
     def upload(self, stream: Optional[torch.cuda.Stream] = None) -> int:
         """Make the schedule device-resident (no-op if already); returns bytes moved."""
@@ -191,7 +196,7 @@ def accum_init(o_accum: torch.Tensor, lse_accum: torch.Tensor, stream=None) -> N
 def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, masks: AttentionMaskSet, *,
                      softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
                      return_lse: bool = False, schedule: Optional[AttentionSchedule] = None,
-                     device_schedule: bool = False):
+                     device_schedule: bool = True):
     """O = softmax(Q K^T * scale) V restricted to the dense 64x64 tiles of
     `masks` (bit (q, k) of head h set => tile computed; reference
     mask.hpp:18-20).  q: [Sq, H, d], k/v: [Sk, H, d], bf16 CUDA, d in {64, 128}.
@@ -211,7 +216,8 @@ def sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, masks: A
         # K2: masks go to the device (1.3 MB for the Wan layer) and the work
         # list is built there; no host pass over the masks, no list upload.
         words = torch.from_numpy(masks.words.view(np.int64)).to(q.device, non_blocking=True)
-        sched = AttentionSchedule().build_device(words, masks.num_kv_blocks, kv_tokens_global=Sk)
+        sched = AttentionSchedule().build_device(words, masks.num_kv_blocks, kv_tokens_global=Sk,
+                                                 head_dim=q.shape[-1])
     elif sched is None:
         sched = AttentionSchedule().build(masks, kv_tokens_global=Sk, head_dim=q.shape[-1])
     sched.launch(q, k, v, out, lse=lse, softmax_scale=softmax_scale)

@@ -14,20 +14,7 @@
 #include <cstdlib>
 
 #include "attn_kernel.cuh"
-#include "attn_kernel_duo.cuh"
-#include "attn_kernel_duo2.cuh"
-#include "attn_kernel_quad.cuh"
-#include "attn_kernel_quadp.cuh"
-#include "attn_kernel_s32.cuh"
-#include "attn_kernel_psmem.cuh"
-#include "attn_kernel_pair.cuh"
-#include "attn_kernel_pd.cuh"
-#include "attn_kernel_pd2.cuh"
 #include "attn_kernel_pd3.cuh"
-#include "attn_kernel_pd4.cuh"
-#include "attn_kernel_pd3p.cuh"
-#include "attn_kernel_split.cuh"
-#include "attn_kernel_wide.cuh"
 #include "capi_util.hpp"
 #include "core.hpp"
 #include "schedule.hpp"
@@ -133,349 +120,22 @@ void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap
   cuda_check(cudaGetLastError(), "sparse_attn_fwd launch");
 }
 
-void launch_wide(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm,
-                 uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::WideCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_wide_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(wide)");
-  dbsp_dev::sparse_attn_fwd_wide_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_wide launch");
-}
-
-template <int D>
-void launch_split(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::KCfg<D>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_split_kernel<D>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(split)");
-  dbsp_dev::sparse_attn_fwd_split_kernel<D>
-      <<<items, dbsp_dev::kThreadsSplit, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_split launch");
-}
-
-// Softmax split across 8 warps (attn_kernel_split.cuh), opt-in (DBSP_K4_SPLIT=1):
-// measured 15.2 ms vs 6.3 ms on the Wan layer (96-register cap at 640
-// threads/SM spills the d=128 softmax) and 1.91 vs 1.85 ms on CogVideoX.
-bool use_split() {
-  static const bool split = [] {
-    const char* e = std::getenv("DBSP_K4_SPLIT");
-    return e && e[0] == '1';
-  }();
-  return split;
-}
-
-void launch_pair(const CUtensorMap& q, const CUtensorMap& k32, const CUtensorMap& v,
-                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::PairCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pair_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(pair)");
-  dbsp_dev::sparse_attn_fwd_pair_kernel<<<2 * items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(
-      q, k32, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pair launch");
-}
-
-// exp2 pairs of every 8 on the FMA pipe in the CTA-pair split-KV kernels
-// (DBSP_PD_POLY=0..3; default 0: attn_kernel_pd3.cuh measured 6.12 / 6.11 /
-// 6.37 ms on Wan with 0 / 1 / 2 of 8, interleaved A/B, tests/ab_probe.py).
-int pd_poly() {
-  static const int n = [] {
-    const char* e = std::getenv("DBSP_PD_POLY");
-    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
-  }();
-  return n;
-}
-
-template <int kPoly>
-void launch_pd_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::PdCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd_kernel<kPoly>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(pd)");
-  dbsp_dev::sparse_attn_fwd_pd_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd, C::kSmemBytes, stream>>>(
-      q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd launch");
-}
-
-template <int kPoly>
-void launch_pd2_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::Pd2Cfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd2_kernel<kPoly>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(pd2)");
-  dbsp_dev::sparse_attn_fwd_pd2_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(
-      q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd2 launch");
-}
-
-template <int kPoly, bool kAlt>
-void launch_pd3_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
+// The CTA-pair split-KV kernel (attn_kernel_pd3.cuh): one cluster of two CTAs
+// per quad item.  No exp2 runs on the FMA pipe at d=128 (kPoly 0): 1 and 2 of
+// 8 pairs measured 6.11 and 6.37 ms against 6.12 ms on Wan (tests/ab_probe.py).
+void launch_pd3(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
   using C = dbsp_dev::Pd3Cfg;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3_kernel<kPoly, kAlt>,
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3_kernel<0>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute(pd3)");
-  dbsp_dev::sparse_attn_fwd_pd3_kernel<kPoly, kAlt>
-      <<<2 * items, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3 launch");
-}
-
-// DBSP_PD_ALT=1: the two stages' exp phases strictly alternate (SmDone).
-bool pd_alt() {
-  static const bool v = [] {
-    const char* e = std::getenv("DBSP_PD_ALT");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-template <int kPoly>
-void launch_pd4_n(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::Pd4Cfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd4_kernel<kPoly>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(pd4)");
-  dbsp_dev::sparse_attn_fwd_pd4_kernel<kPoly><<<2 * items, dbsp_dev::kThreadsPd4, C::kSmemBytes, stream>>>(
+  dbsp_dev::sparse_attn_fwd_pd3_kernel<0><<<2 * items, dbsp_dev::kThreadsPd3, C::kSmemBytes, stream>>>(
       q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd4 launch");
-}
-
-void launch_pd3p(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::Pd3pCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int sms = 148;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3p_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(pd3p)");
-  const uint32_t clusters = std::min<uint32_t>(items, uint32_t(sms / 2));  // one persistent CTA pair per TPC
-  dbsp_dev::sparse_attn_fwd_pd3p_kernel<<<2 * clusters, dbsp_dev::kThreadsPd2, C::kSmemBytes, stream>>>(
-      q, k, v, prm, items);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3p launch");
-}
-
-// Which CTA-pair split-KV kernel runs DBSP_SCHED_CTA_PAIR schedules
-// (DBSP_PD_VARIANT): 1 one softmax warp per row (attn_kernel_pd.cuh),
-// 2 two warps per row (attn_kernel_pd2.cuh), 3 two warps per row with P in
-// shared memory (attn_kernel_pd3.cuh, the default).
-int pd_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("DBSP_PD_VARIANT");
-    return (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 3;
-  }();
-  return v;
-}
-
-void launch_pd(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-               const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  if (pd_variant() == 4) {
-    const int n = pd_poly();
-    if (n == 0) launch_pd4_n<0>(q, k, v, prm, items, stream);
-    else if (n == 1) launch_pd4_n<1>(q, k, v, prm, items, stream);
-    else launch_pd4_n<2>(q, k, v, prm, items, stream);
-    return;
-  }
-  if (pd_variant() == 3) {
-    const int n = pd_poly();
-    if (pd_alt()) {
-      if (n == 0) launch_pd3_n<0, true>(q, k, v, prm, items, stream);
-      else launch_pd3_n<2, true>(q, k, v, prm, items, stream);
-    } else if (n == 1) {
-      launch_pd3_n<1, false>(q, k, v, prm, items, stream);
-    } else if (n >= 2) {
-      launch_pd3_n<2, false>(q, k, v, prm, items, stream);
-    } else {
-      launch_pd3_n<0, false>(q, k, v, prm, items, stream);
-    }
-    return;
-  }
-  if (pd_variant() == 2) {
-    switch (pd_poly()) {
-      case 0: launch_pd2_n<0>(q, k, v, prm, items, stream); break;
-      case 1: launch_pd2_n<1>(q, k, v, prm, items, stream); break;
-      case 3: launch_pd2_n<3>(q, k, v, prm, items, stream); break;
-      default: launch_pd2_n<2>(q, k, v, prm, items, stream); break;
-    }
-    return;
-  }
-  switch (pd_poly()) {
-    case 0: launch_pd_n<0>(q, k, v, prm, items, stream); break;
-    case 1: launch_pd_n<1>(q, k, v, prm, items, stream); break;
-    case 3: launch_pd_n<3>(q, k, v, prm, items, stream); break;
-    default: launch_pd_n<2>(q, k, v, prm, items, stream); break;
-  }
-}
-
-template <int D>
-void launch_duo(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::DuoCfg<D>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo_kernel<D>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(duo)");
-  dbsp_dev::sparse_attn_fwd_duo_kernel<D><<<items, dbsp_dev::kThreadsDuo, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo launch");
-}
-
-template <int D>
-void launch_duo2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::Duo2Cfg<D>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_duo2_kernel<D>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(duo2)");
-  dbsp_dev::sparse_attn_fwd_duo2_kernel<D><<<items, dbsp_dev::kThreadsDuo2, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_duo2 launch");
-}
-
-void launch_quadp(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                  const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::QuadPCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int sms = 148;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_quadp_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(quadp)");
-  const uint32_t grid = std::min<uint32_t>(items, uint32_t(sms));  // one persistent CTA per SM
-  dbsp_dev::sparse_attn_fwd_quadp_kernel<<<grid, dbsp_dev::kThreadsQuadP, C::kSmemBytes, stream>>>(q, k, v, prm,
-                                                                                                  items);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_quadp launch");
-}
-
-template <int D>
-void launch_quad(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
-                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::QuadCfg<D>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_quad_kernel<D>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(quad)");
-  dbsp_dev::sparse_attn_fwd_quad_kernel<D><<<items, dbsp_dev::kThreadsQuad, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_quad launch");
-}
-
-// Quad schedules run the two-stage kernels (64-key steps, or 128-key steps
-// with DBSP_SCHED_KEY128); DBSP_K4_PAIR=1 selects the
-// CTA-pair kernel instead (d=128 only; measured 8.19 ms vs 6.34 ms for the
-// pair-item kernel on the Wan layer).
-bool use_pair() {
-  static const bool pair = [] {
-    const char* e = std::getenv("DBSP_K4_PAIR");
-    return e && e[0] == '1';
-  }();
-  return pair;
-}
-
-void launch_s32(const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm, uint32_t items,
-                cudaStream_t stream) {
-  using C = dbsp_dev::S32Cfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_s32_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(s32)");
-  dbsp_dev::sparse_attn_fwd_s32_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_s32 launch");
-}
-
-void launch_psmem(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v, const dbsp_dev::AttnParams& prm,
-                  uint32_t items, cudaStream_t stream) {
-  using C = dbsp_dev::PsmemCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_psmem_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-  });
-  cuda_check(attr_err, "cudaFuncSetAttribute(psmem)");
-  dbsp_dev::sparse_attn_fwd_psmem_kernel<<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(q, k, v, prm);
-  cuda_check(cudaGetLastError(), "sparse_attn_fwd_psmem launch");
-}
-
-// d=128 with P staged in smem (attn_kernel_psmem.cuh), opt-in.
-bool use_psmem() {
-  static const bool on = [] {
-    const char* e = std::getenv("DBSP_K4_PSMEM");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-// d=128 with Q in TMEM and 32-key sub-steps (attn_kernel_s32.cuh), opt-in.
-bool use_s32() {
-  static const bool s32 = [] {
-    const char* e = std::getenv("DBSP_K4_S32");
-    return e && e[0] == '1';
-  }();
-  return s32;
-}
-
-// d=128 kernel choice.  The 128-key-step variant (one CTA/SM) measured 6.96 ms
-// vs 6.36 ms for the 64-key, two-CTAs-per-SM kernel on the Wan layer: with a
-// single softmax warp per SMSP its softmax cannot hide the MMA completion
-// latency.  Kept selectable (DBSP_K4_WIDE=1) for further work.
-bool use_wide() {
-  static const bool wide = [] {
-    const char* e = std::getenv("DBSP_K4_WIDE");
-    return e && e[0] == '1';
-  }();
-  return wide;
+  cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3 launch");
 }
 
 unsigned long long* g_trace = nullptr;
@@ -493,23 +153,35 @@ struct dbsp_schedule {
   size_t pinned_bytes = 0;
   cudaEvent_t uploaded = nullptr;
   bool pending = false;
-  // device-built schedule (K2): items/entries live only in `dev`
+  // device-built schedule (K2): items/entries live only in `dev`.  With
+  // DBSP_SCHED_AUTO_D128 both lists are built (pair at offset 0, quad at
+  // quad_offset) and `gate` (device u32) says which kernel runs; both are
+  // launched and the other returns at once.
   bool on_device = false;
-  uint32_t dev_items = 0;
-  void* view_dev = nullptr;  // head ids, q ids, present bitmap, kv_local table
+  uint32_t dev_mode = 0;  // 0 pair-item list, 1 CTA-pair (quad) list, 2 both + device choice
+  uint32_t dev_items = 0;      // pair-item list (modes 0, 2)
+  uint32_t dev_quad_items = 0;  // quad list (modes 1, 2)
+  size_t quad_offset = 0, quad_item_bytes = 0;
+  void* view_dev = nullptr;  // head ids, q ids, present bitmap, kv_local table, totals, gate
   size_t view_bytes = 0;
+  uint32_t* gate = nullptr;
+  unsigned long long* totals = nullptr;  // [pair visits, pair dense, quad visits, quad dense]
   void* k2_scratch = nullptr;
   size_t k2_scratch_bytes = 0;
-  unsigned int* item_counter = nullptr;  // persistent kernels: zeroed before each launch
+  // The last launch that reads `dev`: any rewrite of the list (upload, device
+  // build) on another stream waits for it.
+  cudaEvent_t last_use = nullptr;
+  bool used = false;
 
   ~dbsp_schedule() {
     if (pending && uploaded) cudaEventSynchronize(uploaded);
+    if (used && last_use) cudaEventSynchronize(last_use);
+    if (last_use) cudaEventDestroy(last_use);
     if (dev) cudaFree(dev);
     if (pinned) cudaFreeHost(pinned);
     if (uploaded) cudaEventDestroy(uploaded);
     if (view_dev) cudaFree(view_dev);
     if (k2_scratch) cudaFree(k2_scratch);
-    if (item_counter) cudaFree(item_counter);
   }
 };
 
@@ -517,8 +189,10 @@ namespace dbsp_k2 {
 void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global,
            const dbsp_core::LocalView& v, uint32_t flags, const uint32_t* d_head_ids,
            const uint32_t* d_q_ids, const uint64_t* d_present, const int32_t* d_kv_local,
-           dbsp_core::WorkItem* items_out, uint32_t* entries_out, void*& scratch,
-           size_t& scratch_bytes, cudaStream_t stream);
+           dbsp_core::WorkItem* items_out, uint32_t* entries_out, unsigned long long* totals,
+           void*& scratch, size_t& scratch_bytes, cudaStream_t stream);
+void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
+            cudaStream_t stream);
 }
 
 using dbsp_capi::guard;
@@ -527,8 +201,22 @@ namespace {
 
 // Copies items + entries to the device through a pinned staging buffer, on
 // `stream`, only when the host schedule changed since the last upload.
+// Orders a rewrite of sched->dev on `stream` after the last launch that read
+// it (a caller may alternate streams between calls).
+void wait_last_use(dbsp_schedule* sched, cudaStream_t stream) {
+  if (sched->used) cuda_check(cudaStreamWaitEvent(stream, sched->last_use, 0), "wait last use");
+}
+
+void mark_use(dbsp_schedule* sched, cudaStream_t stream) {
+  if (!sched->last_use)
+    cuda_check(cudaEventCreateWithFlags(&sched->last_use, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventRecord(sched->last_use, stream), "event record");
+  sched->used = true;
+}
+
 void upload_schedule(dbsp_schedule* sched, cudaStream_t stream) {
   if (!sched->dirty) return;
+  wait_last_use(sched, stream);
   const Schedule& h = sched->host;
   const size_t item_bytes = h.items.size() * sizeof(WorkItem);
   const size_t bytes = item_bytes + h.entries.size() * sizeof(uint32_t);
@@ -603,10 +291,11 @@ int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
 
 int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, uint32_t heads,
                                uint32_t q_blocks, uint32_t kv_blocks, const dbsp_local_view* view,
-                               int32_t flags, void* stream_ptr) {
+                               int32_t flags_in, void* stream_ptr) {
   return guard([&] {
     if (!sched || !d_words) fail(kContract, "null schedule or mask words");
     if (heads == 0 || q_blocks == 0 || kv_blocks == 0) fail(kConfig, "mask dimensions must be positive");
+    const uint32_t flags = normalize_sched_flags(uint32_t(flags_in));
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     LocalView lv;
     lv.heads = view ? view->num_heads : heads;
@@ -615,6 +304,7 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
     lv.kv_tokens_global = view ? view->kv_tokens_global : 0;
     if (lv.heads == 0 || lv.q_blocks == 0 || lv.kv_blocks == 0)
       fail(kConfig, "local view dimensions must be positive");
+    if (lv.kv_blocks > kEntryKvMask) fail(kConfig, "too many local KV blocks");
     const uint32_t wpr = (kv_blocks + 63) / 64;
     // Host-side view tables (small), uploaded with the build.
     std::vector<uint32_t> hid(lv.heads), qid(lv.q_blocks);
@@ -635,7 +325,15 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
       kvl[k] = int32_t(i);
       present[k / 64] |= 1ull << (k % 64);
     }
-    const size_t vb = hid.size() * 4 + qid.size() * 4 + present.size() * 8 + kvl.size() * 4 + 64;
+    // The previous launch from this schedule may still read the list and the
+    // view tables (it may have run on another stream).
+    wait_last_use(sched, stream);
+    if (sched->pending) {
+      cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
+      sched->pending = false;
+    }
+    // view_dev: present | totals (4 x u64) | gate (u32, padded) | hid | qid | kvl
+    const size_t vb = present.size() * 8 + 32 + 16 + hid.size() * 4 + qid.size() * 4 + kvl.size() * 4 + 64;
     if (sched->view_bytes < vb) {
       if (sched->view_dev) cudaFree(sched->view_dev);
       sched->view_dev = nullptr;
@@ -644,44 +342,91 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
     }
     uint8_t* vd = static_cast<uint8_t*>(sched->view_dev);
     uint64_t* d_present = reinterpret_cast<uint64_t*>(vd);  // 8-byte aligned first
-    uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + present.size() * 8);
+    sched->totals = reinterpret_cast<unsigned long long*>(vd + present.size() * 8);
+    sched->gate = reinterpret_cast<uint32_t*>(vd + present.size() * 8 + 32);
+    uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + present.size() * 8 + 48);
     uint32_t* d_qid = d_hid + hid.size();
     int32_t* d_kvl = reinterpret_cast<int32_t*>(d_qid + qid.size());
     cuda_check(cudaMemcpyAsync(d_present, present.data(), present.size() * 8, cudaMemcpyHostToDevice, stream), "view");
     cuda_check(cudaMemcpyAsync(d_hid, hid.data(), hid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
     cuda_check(cudaMemcpyAsync(d_qid, qid.data(), qid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
     cuda_check(cudaMemcpyAsync(d_kvl, kvl.data(), kvl.size() * 4, cudaMemcpyHostToDevice, stream), "view");
-    const uint32_t step = (flags & kSchedPairQ) ? 2 : 1;
-    const uint32_t n = lv.heads * ((lv.q_blocks + step - 1) / step);
-    const size_t item_bytes = size_t(n) * sizeof(WorkItem);
-    const size_t bytes = item_bytes + size_t(n) * lv.kv_blocks * sizeof(uint32_t);
-    if (sched->pending) {
-      cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
-      sched->pending = false;
-    }
+
+    const bool auto_d128 = (flags & kSchedAutoD128) != 0;
+    const bool quad_only = (flags & kSchedQuad) != 0;
+    const uint32_t keep = flags & (kSchedGlobalLpt | kSchedHeadOrder);
+    const uint32_t pair_flags = auto_d128 ? (keep | kSchedPairQ) : flags;
+    const uint32_t quad_flags = keep | kSchedPairQ | kSchedQuad | kSchedKey128 | kSchedCtaPair;
+    const uint32_t pstep = (pair_flags & kSchedPairQ) ? 2 : 1;
+    const uint32_t n_pair = quad_only ? 0 : lv.heads * ((lv.q_blocks + pstep - 1) / pstep);
+    const uint32_t n_quad = (quad_only || auto_d128) ? lv.heads * ((lv.q_blocks + 3) / 4) : 0;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t pair_item_bytes = size_t(n_pair) * sizeof(WorkItem);
+    const size_t pair_bytes = al(pair_item_bytes + size_t(n_pair) * lv.kv_blocks * sizeof(uint32_t));
+    const size_t quad_item_bytes = size_t(n_quad) * sizeof(WorkItem);
+    const size_t bytes = pair_bytes + quad_item_bytes + size_t(n_quad) * lv.kv_blocks * sizeof(uint32_t);
     if (sched->dev_bytes < bytes) {
       if (sched->dev) cudaFree(sched->dev);
       sched->dev = nullptr;
       cuda_check(cudaMalloc(&sched->dev, bytes), "cudaMalloc schedule");
       sched->dev_bytes = bytes;
     }
-    dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, uint32_t(flags), d_hid, d_qid, d_present, d_kvl,
-                   static_cast<WorkItem*>(sched->dev),
-                   reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(sched->dev) + item_bytes),
-                   sched->k2_scratch, sched->k2_scratch_bytes, stream);
+    uint8_t* base = static_cast<uint8_t*>(sched->dev);
+    if (n_pair)
+      dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, pair_flags, d_hid, d_qid, d_present, d_kvl,
+                     reinterpret_cast<WorkItem*>(base), reinterpret_cast<uint32_t*>(base + pair_item_bytes),
+                     auto_d128 ? sched->totals : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream);
+    if (n_quad)
+      dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, quad_flags, d_hid, d_qid, d_present, d_kvl,
+                     reinterpret_cast<WorkItem*>(base + pair_bytes),
+                     reinterpret_cast<uint32_t*>(base + pair_bytes + quad_item_bytes),
+                     auto_d128 ? sched->totals + 2 : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream);
+    if (auto_d128) dbsp_k2::choose(sched->totals, sched->totals + 2, sched->gate, stream);
     // Bounds for the launch-time checks; the host copy of the list is empty.
     sched->host.items.clear();
     sched->host.entries.clear();
     sched->host.tile_visits = sched->host.dense_tiles = 0;
+    sched->host.flags = flags;
     sched->host.max_head = lv.heads - 1;
     sched->host.max_q_block = lv.q_blocks - 1;
     sched->host.max_kv_block = lv.kv_blocks - 1;
     sched->on_device = true;
     sched->dirty = false;
-    sched->dev_items = n;
-    sched->item_bytes = item_bytes;
+    sched->dev_mode = auto_d128 ? 2u : quad_only ? 1u : 0u;
+    sched->dev_items = n_pair;
+    sched->item_bytes = pair_item_bytes;
+    sched->dev_quad_items = n_quad;
+    sched->quad_offset = pair_bytes;
+    sched->quad_item_bytes = quad_item_bytes;
   });
 }
+
+namespace {
+// The list a device-built schedule runs: quad (CTA-pair) or pair items.
+bool device_runs_quad(const dbsp_schedule* s) {
+  if (s->dev_mode != 2) return s->dev_mode == 1;
+  uint32_t g = 0;
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  cuda_check(cudaMemcpy(&g, s->gate, 4, cudaMemcpyDeviceToHost), "d2h gate");
+  return g != 0;
+}
+
+// Device-built list (chosen layout) read back to host; diagnostics only.
+void download_device(const dbsp_schedule* s, std::vector<WorkItem>& items, std::vector<uint32_t>& entries,
+                     bool& quad) {
+  quad = device_runs_quad(s);
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  const uint8_t* base = static_cast<const uint8_t*>(s->dev) + (quad ? s->quad_offset : 0);
+  const uint32_t n_items = quad ? s->dev_quad_items : s->dev_items;
+  const size_t ib = quad ? s->quad_item_bytes : s->item_bytes;
+  items.resize(n_items);
+  if (n_items) cuda_check(cudaMemcpy(items.data(), base, ib, cudaMemcpyDeviceToHost), "d2h");
+  uint64_t n = 0;
+  for (const WorkItem& w : items) n += w.count;
+  entries.resize(n);
+  if (n) cuda_check(cudaMemcpy(entries.data(), base + ib, n * 4, cudaMemcpyDeviceToHost), "d2h");
+}
+}  // namespace
 
 int dbsp_schedule_stats(const dbsp_schedule* s, uint64_t* items, uint64_t* visits,
                         uint64_t* dense) {
@@ -693,20 +438,15 @@ int dbsp_schedule_stats(const dbsp_schedule* s, uint64_t* items, uint64_t* visit
       if (dense) *dense = s->host.dense_tiles;
       return;
     }
-    // Device-built: read the list back (synchronous; diagnostics only).
-    cuda_check(cudaDeviceSynchronize(), "sync");
-    std::vector<WorkItem> it(s->dev_items);
-    cuda_check(cudaMemcpy(it.data(), s->dev, it.size() * sizeof(WorkItem), cudaMemcpyDeviceToHost), "d2h");
-    uint64_t n = 0;
-    for (const WorkItem& w : it) n += w.count;
-    std::vector<uint32_t> e(n);
-    if (n)
-      cuda_check(cudaMemcpy(e.data(), static_cast<uint8_t*>(s->dev) + s->item_bytes, n * 4,
-                            cudaMemcpyDeviceToHost), "d2h");
+    std::vector<WorkItem> it;
+    std::vector<uint32_t> e;
+    bool quad = false;
+    download_device(s, it, e, quad);
+    const uint32_t dmask = quad ? (0xFu << 22) : (kEntryDenseA | kEntryDenseB);
     uint64_t dn = 0;
-    for (uint32_t x : e) dn += ((x & kEntryDenseA) != 0) + ((x & kEntryDenseB) != 0);
-    if (items) *items = s->dev_items;
-    if (visits) *visits = n;
+    for (uint32_t x : e) dn += __builtin_popcount(x & dmask);
+    if (items) *items = it.size();
+    if (visits) *visits = e.size();
     if (dense) *dense = dn;
   });
 }
@@ -714,7 +454,13 @@ int dbsp_schedule_stats(const dbsp_schedule* s, uint64_t* items, uint64_t* visit
 int dbsp_schedule_layout(const dbsp_schedule* s, uint32_t* flags) {
   return guard([&] {
     if (!s || !flags) fail(kContract, "null argument");
-    *flags = s->on_device ? uint32_t(kSchedPairQ) : s->host.flags;  // K2 builds pair schedules
+    if (!s->on_device) {
+      *flags = s->host.flags;
+      return;
+    }
+    const uint32_t order = s->host.flags & (kSchedGlobalLpt | kSchedHeadOrder);
+    *flags = device_runs_quad(s) ? (order | kSchedPairQ | kSchedQuad | kSchedKey128 | kSchedCtaPair)
+                                 : (order | (s->host.flags & kSchedPairQ));
   });
 }
 
@@ -728,14 +474,13 @@ int dbsp_schedule_download(const dbsp_schedule* s, void* items_out, uint32_t* en
       if (entries_out) std::memcpy(entries_out, s->host.entries.data(), s->host.entries.size() * 4);
       return;
     }
-    cuda_check(cudaDeviceSynchronize(), "sync");
-    cuda_check(cudaMemcpy(items_out, s->dev, size_t(s->dev_items) * sizeof(WorkItem), cudaMemcpyDeviceToHost), "d2h");
-    uint64_t n = 0;
-    for (uint32_t i = 0; i < s->dev_items; ++i) n += static_cast<const WorkItem*>(items_out)[i].count;
-    if (n > max_entries) fail(kContract, "entries buffer too small");
-    if (entries_out && n)
-      cuda_check(cudaMemcpy(entries_out, static_cast<uint8_t*>(s->dev) + s->item_bytes, n * 4,
-                            cudaMemcpyDeviceToHost), "d2h");
+    std::vector<WorkItem> it;
+    std::vector<uint32_t> e;
+    bool quad = false;
+    download_device(s, it, e, quad);
+    std::memcpy(items_out, it.data(), it.size() * sizeof(WorkItem));
+    if (e.size() > max_entries) fail(kContract, "entries buffer too small");
+    if (entries_out && !e.empty()) std::memcpy(entries_out, e.data(), e.size() * 4);
   });
 }
 
@@ -770,7 +515,8 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       fail(kContract, "incomplete output scatter");
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     const Schedule& h = sched->host;
-    const uint32_t n_items = sched->on_device ? sched->dev_items : uint32_t(h.items.size());
+    const uint32_t n_items = sched->on_device ? sched->dev_items + sched->dev_quad_items
+                                              : uint32_t(h.items.size());
     if (n_items == 0) return;
     const uint32_t q_blocks = (a->q_tokens + 63) / 64, kv_blocks = (a->kv_tokens + 63) / 64;
     if (h.max_head >= a->heads || h.max_q_block >= q_blocks)
@@ -783,6 +529,8 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
     prm.items = static_cast<const WorkItem*>(sched->dev);
     prm.entries =
         reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(sched->dev) + sched->item_bytes);
+    prm.gate = nullptr;
+    prm.gate_value = 0;
     prm.q = static_cast<const __nv_bfloat16*>(a->q);
     prm.out = static_cast<__nv_bfloat16*>(a->o);
     prm.lse = a->lse;
@@ -799,61 +547,42 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
     prm.scatter_rows = sc ? sc->q_block_map : nullptr;
     prm.scatter_heads = sc ? sc->head_map : nullptr;
     prm.out_heads = sc ? sc->out_heads : 0;
-    prm.item_counter = nullptr;
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
-    const bool quad = !sched->on_device && (h.flags & kSchedQuad);
-    if (quad && use_pair() && a->head_dim != 128) fail(kConfig, "the CTA-pair kernel needs head_dim 128");
-    if (sc && ((quad && use_pair()) || (!quad && (use_wide() || use_split()))))
-      fail(kConfig, "the fused O return is not available in the opt-in pair/wide/split kernels");
-    if (quad && use_pair())
-      launch_pair(tq, make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim, 32), tv, prm, n_items, stream);
-    else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedCtaPair)) {
-      if (a->head_dim != 128) fail(kConfig, "the CTA-pair split-KV kernel needs head_dim 128");
-      if (h.flags & kSchedPersist) {
-        if (!sched->item_counter)
-          cuda_check(cudaMalloc(&sched->item_counter, sizeof(unsigned int)), "cudaMalloc item counter");
-        cuda_check(cudaMemsetAsync(sched->item_counter, 0, sizeof(unsigned int), stream), "memset item counter");
-        prm.item_counter = sched->item_counter;
-        launch_pd3p(tq, tk, tv, prm, n_items, stream);
+    if (!sched->on_device) {
+      if (h.flags & kSchedQuad) {
+        if (a->head_dim != 128) fail(kConfig, "the CTA-pair kernel (quad schedules) needs head_dim 128");
+        launch_pd3(tq, tk, tv, prm, n_items, stream);
+      } else if (a->head_dim == 128) {
+        launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
       } else {
-        launch_pd(tq, tk, tv, prm, n_items, stream);
+        launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
       }
-    } else if (quad && (h.flags & kSchedKey128) && (h.flags & kSchedSplitSoftmax)) {
-      if (a->head_dim == 128)
-        launch_duo2<128>(tq, tk, tv, prm, n_items, stream);
-      else
-        launch_duo2<64>(tq, tk, tv, prm, n_items, stream);
-    } else if (quad && (h.flags & kSchedKey128) && a->head_dim == 128)
-      launch_duo<128>(tq, tk, tv, prm, n_items, stream);
-    else if (quad && (h.flags & kSchedKey128))
-      launch_duo<64>(tq, tk, tv, prm, n_items, stream);
-    else if (quad && (h.flags & kSchedPersist) && a->head_dim == 128) {
-      if (!sched->item_counter)
-        cuda_check(cudaMalloc(&sched->item_counter, sizeof(unsigned int)), "cudaMalloc item counter");
-      cuda_check(cudaMemsetAsync(sched->item_counter, 0, sizeof(unsigned int), stream), "memset item counter");
-      prm.item_counter = sched->item_counter;
-      launch_quadp(tq, tk, tv, prm, n_items, stream);
+    } else {
+      // Device-built list(s).  Mode 2 launches both kernels, each gated on
+      // the device-side choice (k2_choose); the other returns at once.
+      if (sched->dev_mode != 0 && a->head_dim != 128)
+        fail(kConfig, "the CTA-pair kernel (quad schedules) needs head_dim 128");
+      const bool gated = sched->dev_mode == 2;
+      if (sched->dev_mode != 1 && sched->dev_items) {
+        prm.gate = gated ? sched->gate : nullptr;
+        prm.gate_value = 0;
+        if (a->head_dim == 128)
+          launch_kernel<128>(tq, tk, tv, prm, sched->dev_items, stream);
+        else
+          launch_kernel<64>(tq, tk, tv, prm, sched->dev_items, stream);
+      }
+      if (sched->dev_mode != 0 && sched->dev_quad_items) {
+        const uint8_t* qb = static_cast<const uint8_t*>(sched->dev) + sched->quad_offset;
+        prm.items = reinterpret_cast<const WorkItem*>(qb);
+        prm.entries = reinterpret_cast<const uint32_t*>(qb + sched->quad_item_bytes);
+        prm.gate = gated ? sched->gate : nullptr;
+        prm.gate_value = 1;
+        launch_pd3(tq, tk, tv, prm, sched->dev_quad_items, stream);
+      }
     }
-    else if (quad && a->head_dim == 128)
-      launch_quad<128>(tq, tk, tv, prm, n_items, stream);
-    else if (quad)
-      launch_quad<64>(tq, tk, tv, prm, n_items, stream);
-    else if (a->head_dim == 128 && use_psmem())
-      launch_psmem(tq, tk, tv, prm, n_items, stream);
-    else if (a->head_dim == 128 && use_s32())
-      launch_s32(tk, tv, prm, n_items, stream);
-    else if (a->head_dim == 128 && use_wide())
-      launch_wide(tk, tv, prm, n_items, stream);
-    else if (use_split() && a->head_dim == 128)
-      launch_split<128>(tq, tk, tv, prm, n_items, stream);
-    else if (use_split())
-      launch_split<64>(tq, tk, tv, prm, n_items, stream);
-    else if (a->head_dim == 128)
-      launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
-    else
-      launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
+    mark_use(sched, stream);
   }
 }
 }  // namespace
@@ -871,24 +600,57 @@ int dbsp_attention_launch_scatter(dbsp_schedule* sched, const dbsp_attn_args* a,
 }
 
 int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, void* stream) {
-  static thread_local dbsp_schedule* sched = nullptr;
-  if (!sched) {
-    const int rc = dbsp_schedule_create(&sched);
-    if (rc) return rc;
-  }
+  // One schedule and one device copy of the mask words per thread, reused by
+  // every call.  The words go to the device (1.3 MB for the Wan layer) and K2
+  // builds the list there -- for d=128 both layouts plus the device-side
+  // choice (DBSP_SCHED_AUTO_D128) -- so a call with fresh masks costs no host
+  // pass over the masks.
+  struct OneShot {
+    dbsp_schedule* sched = nullptr;
+    uint64_t* words = nullptr;
+    size_t cap = 0;
+    ~OneShot() {
+      if (sched) dbsp_schedule_destroy(sched);  // waits for the last launch
+      if (words) cudaFree(words);
+    }
+  };
+  static thread_local OneShot os;
   dbsp_local_view v;
-  std::memset(&v, 0, sizeof(v));
-  if (set) {
+  int32_t flags = 0;
+  int rc = guard([&] {
+    if (!set || !args) fail(kContract, "null mask set or args");
+    if (!set->heads) fail(kContract, "null mask rows");
+    if (set->num_heads == 0 || set->num_q_blocks == 0 || set->num_kv_blocks == 0)
+      fail(kConfig, "mask dimensions must be positive");
+    if (!os.sched) os.sched = new dbsp_schedule();
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t wpr = (set->num_kv_blocks + 63) / 64;
+    const size_t per_head = size_t(set->num_q_blocks) * wpr;
+    const size_t bytes = per_head * set->num_heads * sizeof(uint64_t);
+    wait_last_use(os.sched, st);  // the previous call's K2 read the words
+    if (os.cap < bytes) {
+      if (os.words) cudaFree(os.words);
+      os.words = nullptr;
+      cuda_check(cudaMalloc(&os.words, bytes), "cudaMalloc mask words");
+      os.cap = bytes;
+    }
+    for (uint32_t h = 0; h < set->num_heads; ++h) {
+      if (!set->heads[h]) fail(kContract, "null mask rows");
+      cuda_check(cudaMemcpyAsync(os.words + h * per_head, set->heads[h], per_head * sizeof(uint64_t),
+                                 cudaMemcpyHostToDevice, st), "mask words H2D");
+    }
+    std::memset(&v, 0, sizeof(v));
     v.num_heads = set->num_heads;
     v.num_q_blocks = set->num_q_blocks;
     v.num_kv_blocks = set->num_kv_blocks;
-    v.kv_tokens_global = args ? args->kv_tokens : 0;
-  }
-  // pair schedule; for d=128 the CTA-pair kernel where its quads stay dense
-  const int32_t flags = (args && args->head_dim == 128) ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : 1;
-  const int rc = dbsp_schedule_build(sched, set, &v, flags);
+    v.kv_tokens_global = args->kv_tokens;
+    flags = args->head_dim == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : DBSP_SCHED_PAIR_Q;
+  });
   if (rc) return rc;
-  return dbsp_attention_launch(sched, args, stream);
+  rc = dbsp_schedule_build_device(os.sched, os.words, set->num_heads, set->num_q_blocks, set->num_kv_blocks,
+                                  &v, flags, stream);
+  if (rc) return rc;
+  return dbsp_attention_launch(os.sched, args, stream);
 }
 
 // Debug hook (not in the public header): device buffer of 16 blocks x 256

@@ -61,9 +61,16 @@ struct AttnParams {
   const uint32_t* scatter_rows;
   const uint32_t* scatter_heads;
   uint32_t out_heads;
-  // Persistent kernels: work-item counter, zeroed before each launch.
-  unsigned int* item_counter;
+  // Device-side kernel choice (a K2 build with DBSP_SCHED_AUTO_D128): when
+  // non-null, the kernel runs only if *gate == gate_value; otherwise every CTA
+  // returns before touching shared memory, TMEM or a cluster barrier.
+  const uint32_t* gate;
+  uint32_t gate_value;
 };
+
+__device__ __forceinline__ bool gated_off(const AttnParams& p) {
+  return p.gate != nullptr && *p.gate != p.gate_value;
+}
 
 // Where the bf16 output row of (local token, local head) goes: the local
 // buffer, or its home rank's buffer when the O return is fused (out_peers).
@@ -236,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  if (gated_off(p)) return;  // the device-side choice picked the other kernel
   using C = KCfg<D>;
   constexpr int NS = C::kStages;
   constexpr int NSB = C::kNSB;

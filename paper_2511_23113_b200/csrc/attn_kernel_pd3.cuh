@@ -1,33 +1,77 @@
 // K4, d=128: CTA pair (tcgen05 cta_group::2) x two split-KV stages per CTA,
 // two softmax warps per row, P staged in shared memory.
 //
-// attn_kernel_pd2.cuh writes the bf16 P over S in TMEM, so each stage's step
-// is a serial chain: softmax(t) -> PV(t) -> QK^T(t+2) into the same columns ->
-// softmax(t+2).  Traced (tests/trace_kernel.py --sched 153): softmax ~2150 +
-// hand-off ~250 + the stage's own MMAs ~1024 + latency = a ~3800-cycle period
-// per two steps against 2048 cycles of tensor work.  Here the softmax warps
-// release S(t) as soon as they have read it (Sfree), write P(t) to a
-// shared-memory tile in the 128-byte-swizzled K-major layout, and the leader
-// issues QK^T(t+2) right after Sfree(t), ahead of PV(t) (SS mode: A = P from
-// smem).  The MMAs leave the chain; what remains per stage is the softmax.
-// Cost: per 128-key step an SM writes and the tensor core reads 32 KB of P
-// (160 KB through the port per 1024 tensor cycles instead of 96 KB).
-// The O rescale and the P(t) store wait for PV(t-2) (Pempty), which S(t)'s
+// A cluster of two CTAs on the two SMs of a TPC runs one quad work item
+// (schedule.hpp kSchedQuad|kSchedKey128|kSchedCtaPair): four 64-row Q blocks
+// of one head, CTA rank r owning blocks 2r, 2r+1 (128 rows), against the union
+// of their dense KV blocks, walked in 128-key steps (two entries per step).
+// The steps alternate between two stages of each CTA -- stage 0 takes the even
+// steps, stage 1 the odd ones -- each with its own S and O in TMEM and its own
+// running (m, l); the epilogue merges the two partial results row by row.
+//
+// The leader CTA issues M=256 N=128 MMAs for both CTAs:
+//   S_s = Q K^T   SS  A: each CTA's own Q (smem); B: CTA r holds the 64 keys
+//                     of entry 2t+r (one KV block)
+//   O_s += P_s V  SS  A: each CTA's own P (smem, written by the softmax);
+//                     B: CTA r holds columns [64r, 64r+64) of V, 128 keys
+// Each SM stages only its half of every K / V step, so the B operand bytes per
+// SM are half those of a one-CTA M=128 tile.
+//
+// The softmax warps release S(t) as soon as they have read it (Sfree), write
+// P(t) to a shared-memory tile in the 128-byte-swizzled K-major layout, and
+// the leader issues QK^T(t+2) right after Sfree(t), ahead of PV(t).  The MMAs
+// leave the per-stage chain; what remains per stage is the softmax.  The O
+// rescale and the P(t) store wait for PV(t-2) (Pempty), which S(t)'s
 // completion no longer implies.
-// Warp roles, TMEM and the epilogue are those of attn_kernel_pd2.cuh.
+//
+// Every row's softmax is shared by two warps (one per 64-key block of the
+// step).  They exchange their partial row max through shared memory and a
+// 64-thread named barrier, so both use the same running max m (same lazy
+// rescale decision); each keeps the partial row sum of its half.
+// Warp roles (640 threads, five warpgroups, one CTA per SM):
+//   WG0..WG3 (warps 0-15)  softmax + epilogue; warp w: stage w/8, key half
+//                          (w/4)%2, TMEM lanes 32*(w%4).  setmaxnreg 104.
+//   WG4: warp 16 TMA producer (both CTAs), warp 17 TMEM owner + MMA issuer
+//        (leader), warps 18-19 idle.  setmaxnreg 64.
+// Epilogue: the four threads of a row (stage x half) exchange (m, l) and each
+// writes 32 of the 128 output columns of O = (a0 O_0 + a1 O_1) / L.
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
+// The design history (one warp per row, P over S in TMEM, persistence, ...)
+// with the measured numbers of each rejected variant is in DESIGN.md §3 and
+// profiles/README.md.
 // Mask semantics follow the reference BlockMask (mask.hpp:18-20).
 #pragma once
 
-#include "attn_kernel_pd.cuh"
+#include "attn_kernel.cuh"
 
 namespace dbsp_dev {
 
-// DBSP_TRACE_MMA: the leader's MMA thread per step t -- 0 Sfree(t) seen,
-// 1 QK^T(t+2) issued, 2 Pfull(t) seen, 3 Vfull(t) seen, 4 PV(t) issued,
-// 5 Kfull(t+2) seen.
-#ifdef DBSP_TRACE_MMA
+constexpr int kThreadsPd3 = 640;
+
+// DBSP_TRACE builds (tests/trace_kernel.py): DBSP_TRACE_FINE records the
+// stage-0 softmax phases, DBSP_TRACE_MMA the leader's MMA thread, the default
+// trace the per-stage step boundaries.
+#if defined(DBSP_TRACE_MMA)
+#define PD_TR(ev, j) \
+  do {               \
+  } while (0)
+#define PD_TRC(ev, j) \
+  do {                \
+  } while (0)
 #define PD_TRM(ev, j) DBSP_TR(ev, j)
+#elif defined(DBSP_TRACE_FINE)
+#define PD_TR(ev, j) DBSP_TR(ev, j)
+#define PD_TRC(ev, j) \
+  do {                \
+  } while (0)
+#define PD_TRM(ev, j) \
+  do {                \
+  } while (0)
 #else
+#define PD_TR(ev, j) \
+  do {               \
+  } while (0)
+#define PD_TRC(ev, j) DBSP_TR(ev, j)
 #define PD_TRM(ev, j) \
   do {                \
   } while (0)
@@ -50,11 +94,12 @@ struct Pd3Cfg {
       kQBytes + kStages * (kKStep + kVStep) + 2 * kPBytes + kXBytes + kMlBytes + 1024 + 8 * kNumBars + 16;
 };
 
-template <int kPoly, bool kAltExp>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
+template <int kPoly>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
     sparse_attn_fwd_pd3_kernel(const __grid_constant__ CUtensorMap tmQ,
                                const __grid_constant__ CUtensorMap tmK,
                                const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  if (gated_off(p)) return;  // the device-side choice picked the other kernel
   using C = Pd3Cfg;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -77,8 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
   auto bPfull = [&](int st) { return sBar + 8u * (4 * NS + 2 + st); };
   const uint32_t bQ = sBar + 8u * (4 * NS + 4);
   const uint32_t bOfinal = sBar + 8u * (4 * NS + 5);
-  // exp phases run in step order across the two stages (one phase per step)
-  auto bSmDone = [&](int st) { return sBar + 8u * (4 * NS + 6 + st); };
+  // slots 4*NS+6, 4*NS+7 are unused (kept so the barrier layout matches the traces in profiles/)
   auto bSfree = [&](int st) { return sBar + 8u * (4 * NS + 8 + st); };   // S_st read (leader)
   auto bPempty = [&](int st) { return sBar + 8u * (4 * NS + 10 + st); };  // PV_st done (both CTAs)
   const uint32_t sTmemSlot = sBar + 8u * C::kNumBars;
@@ -106,8 +150,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
     }
     mbar_init(bQ, 1);
     mbar_init(bOfinal, 1);
-    mbar_init(bSmDone(0), 8);  // the stage's softmax warps of this CTA
-    mbar_init(bSmDone(1), 8);
     for (int st = 0; st < 2; ++st) {
       mbar_init(bSfree(st), 16);  // 8 softmax warps of the stage in each CTA of the pair
       mbar_init(bPempty(st), 1);
@@ -313,11 +355,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
           tc_fence_after();
         }
       };
-      // Optional strict alternation of the two stages' exp phases.
-      auto wait_turn = [&]() {
-        if (kAltExp && t > 0) mbar_wait(bSmDone(1 - st), ((t - 1) >> 1) & 1);
-        if (tr0) PD_TR(3, t >> 1);
-      };
       // Pass 1 reads S for the row max, pass 2 again for the exps: holding the
       // 64 values across the max exchange instead (one read, S released before
       // the exchange) spills at 104 registers and measured 1.8x slower.
@@ -353,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
       if (dense) {
         load_s(v);  // pass 2
         release_s();
-        wait_turn();
+        if (tr0) PD_TR(3, t >> 1);
         wait_pv();
         const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
         float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -382,13 +419,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd2, 1)
         l += a2.x + a2.y;
       } else {
         release_s();
-        wait_turn();
+        if (tr0) PD_TR(3, t >> 1);
         wait_pv();
 #pragma unroll
         for (int u = 0; u < 8; ++u) *reinterpret_cast<uint4*>(prow + ((u ^ (row & 7)) << 4)) = make_uint4(0, 0, 0, 0);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bSmDone(st));
       if (tr0) PD_TR(4, t >> 1);
       if (__any_sync(0xffffffffu, need_o)) {
         // O_s is quiescent: PV_s(t-2) completed (wait_pv).

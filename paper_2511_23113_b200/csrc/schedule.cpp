@@ -7,7 +7,18 @@
 
 namespace dbsp_core {
 
+uint32_t normalize_sched_flags(uint32_t flags) {
+  if (flags & ~kSchedKnown) fail(kConfig, "unknown schedule flag bits");
+  if (flags & kSchedCtaPair) flags |= kSchedPairQ | kSchedQuad | kSchedKey128;
+  else if (flags & (kSchedQuad | kSchedKey128))
+    fail(kConfig, "quad / 128-key layouts run only the CTA-pair kernel: pass DBSP_SCHED_CTA_PAIR");
+  if ((flags & kSchedAutoD128) && (flags & kSchedCtaPair))
+    fail(kConfig, "DBSP_SCHED_AUTO_D128 chooses the layout itself; do not combine it with CTA_PAIR");
+  return flags;
+}
+
 void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out) {
+  flags = normalize_sched_flags(flags);
   if (flags & kSchedAutoD128) {
     const uint32_t keep = flags & (kSchedGlobalLpt | kSchedHeadOrder);
     Schedule quad;

@@ -54,11 +54,9 @@ struct Schedule {
 constexpr uint32_t kSchedPairQ = 1;      // two Q blocks per 128-row tile
 constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all heads
 constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
-constexpr uint32_t kSchedQuad = 8;       // four Q blocks per item (two-stage kernels)
-constexpr uint32_t kSchedKey128 = 16;    // with kSchedQuad: 128-key steps (attn_kernel_duo.cuh)
-constexpr uint32_t kSchedPersist = 64;  // with kSchedQuad, d=128: persistent quad kernel (attn_kernel_quadp.cuh)
-constexpr uint32_t kSchedSplitSoftmax = 32;  // with kSchedQuad|kSchedKey128, d=128: attn_kernel_duo2.cuh
-constexpr uint32_t kSchedCtaPair = 128;  // with kSchedQuad|kSchedKey128, d=128: attn_kernel_pd3.cuh
+constexpr uint32_t kSchedQuad = 8;       // layout: four Q blocks per item
+constexpr uint32_t kSchedKey128 = 16;    // layout: 128-key steps
+constexpr uint32_t kSchedCtaPair = 128;  // d=128 CTA-pair kernel (attn_kernel_pd3.cuh); implies 1|8|16
 // For head_dim 128: build the CTA-pair quad schedule (kSchedPairQ|kSchedQuad|
 // kSchedKey128|kSchedCtaPair) when its dense fraction is at least
 // kAutoQuadRatio of the pair schedule's, else the pair schedule.  The
@@ -66,7 +64,12 @@ constexpr uint32_t kSchedCtaPair = 128;  // with kSchedQuad|kSchedKey128, d=128:
 // share their KV blocks (Wan, HunyuanVideo, banded masks: 0.96-0.99 dense vs
 // 0.99-1.00 for pairs) and 1.23x slower on uniform random masks (0.41 vs 0.60).
 constexpr uint32_t kSchedAutoD128 = 256;
+constexpr uint32_t kSchedKnown = kSchedPairQ | kSchedGlobalLpt | kSchedHeadOrder | kSchedQuad | kSchedKey128 |
+                                 kSchedCtaPair | kSchedAutoD128;
 constexpr double kAutoQuadRatio = 0.95;
+// Flags as built: CTA_PAIR implies the quad layout bits; QUAD / KEY128 alone
+// (the retired two-stage one-CTA kernels) and unknown bits are config errors.
+uint32_t normalize_sched_flags(uint32_t flags);
 // Quad items: WorkItem{head, q0, q1, begin, count, pad_mask, q2, q3}; entries
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
 constexpr uint32_t kQuadValidShift = 26;

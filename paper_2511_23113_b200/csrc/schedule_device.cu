@@ -32,32 +32,74 @@ struct K2Args {
   const int32_t* kv_local;    // [nk_global] global KV block -> local index or -1
   uint32_t kv_tokens_global;  // 0 = all blocks full
   uint32_t items_per_head;
-  uint32_t step;              // 2 = paired Q blocks
+  uint32_t step;              // 1, 2 (paired Q blocks) or 4 (quad items of the CTA-pair kernel)
   uint32_t head_order;        // 1 = per-head LPT, 0 = global LPT
 };
 
-__device__ __forceinline__ void item_rows(const K2Args& a, uint32_t i, uint32_t& hl, uint32_t& qa,
-                                          uint32_t& qb, bool& single) {
-  hl = i / a.items_per_head;
-  qa = (i % a.items_per_head) * a.step;
-  single = a.step == 1 || qa + 1 >= a.nq_local;
-  qb = single ? qa : qa + 1;
+// The Q rows of item i (schedule.cpp): local head, up to four local Q blocks
+// (padded rows repeat the first block and set bit r of `pad`).
+struct ItemRows {
+  uint32_t hl, q[4], pad, n;
+  const uint64_t* row[4];
+};
+
+__device__ __forceinline__ ItemRows item_rows(const K2Args& a, uint32_t i) {
+  ItemRows r;
+  r.hl = i / a.items_per_head;
+  const uint32_t q0 = (i % a.items_per_head) * a.step;
+  const uint32_t h = a.head_ids[r.hl];
+  r.pad = 0;
+  r.n = a.step;
+#pragma unroll
+  for (uint32_t j = 0; j < 4; ++j) {
+    const bool in = j < a.step && q0 + j < a.nq_local;
+    r.q[j] = in ? q0 + j : q0;
+    r.row[j] = in ? a.words + (size_t(h) * a.nq_global + a.q_ids[q0 + j]) * a.wpr : nullptr;
+    if (!in && j < a.step) r.pad |= 1u << j;
+  }
+  return r;
 }
 
-__global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned long long* keys) {
+__device__ __forceinline__ uint64_t row_word(const ItemRows& r, uint32_t j, uint32_t w) {
+  return r.row[j] ? r.row[j][w] : 0ull;
+}
+
+// totals: [0] tile visits (sum of counts), [1] dense 64x64 tiles -- the inputs
+// of the DBSP_SCHED_AUTO_D128 choice.
+__global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned long long* keys,
+                         unsigned long long* totals) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_items) return;
-  uint32_t hl, qa, qb;
-  bool single;
-  item_rows(a, i, hl, qa, qb, single);
-  const uint32_t h = a.head_ids[hl];
-  const uint64_t* ra = a.words + (size_t(h) * a.nq_global + a.q_ids[qa]) * a.wpr;
-  const uint64_t* rb = a.words + (size_t(h) * a.nq_global + a.q_ids[qb]) * a.wpr;
-  uint32_t c = 0;
-  for (uint32_t w = 0; w < a.wpr; ++w) c += __popcll((ra[w] | (single ? 0ull : rb[w])) & a.present[w]);
-  counts[i] = c;
-  const unsigned long long head_key = a.head_order ? (unsigned long long)hl : 0ull;
-  keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
+  uint32_t c = 0, dn = 0;
+  if (i < n_items) {
+    const ItemRows r = item_rows(a, i);
+    for (uint32_t w = 0; w < a.wpr; ++w) {
+      const uint64_t p = a.present[w];
+      uint64_t uni = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < 4; ++j) {
+        const uint64_t x = row_word(r, j, w) & p;
+        uni |= x;
+        dn += __popcll(x);
+      }
+      c += __popcll(uni);
+    }
+    counts[i] = c;
+    const unsigned long long head_key = a.head_order ? (unsigned long long)r.hl : 0ull;
+    keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
+  }
+  if (totals) {
+    // warp-aggregated: one atomic pair per warp
+    unsigned long long cv = c, dv = dn;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      cv += __shfl_xor_sync(0xffffffffu, cv, o);
+      dv += __shfl_xor_sync(0xffffffffu, dv, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (cv | dv)) {
+      atomicAdd(totals, cv);
+      atomicAdd(totals + 1, dv);
+    }
+  }
 }
 
 __global__ void k2_sorted_counts(const unsigned long long* sorted_keys, const uint32_t* counts,
@@ -73,18 +115,23 @@ __global__ void k2_write(K2Args a, uint32_t n_items, const unsigned long long* s
   const uint32_t lane = threadIdx.x & 31;
   if (j >= n_items) return;
   const uint32_t i = uint32_t(sorted_keys[j] & 0xFFFFFFull);
-  uint32_t hl, qa, qb;
-  bool single;
-  item_rows(a, i, hl, qa, qb, single);
+  const ItemRows r = item_rows(a, i);
+  const bool quad = a.step == 4;
   const uint32_t begin = begins[j];
-  if (lane == 0) items[j] = WorkItem{hl, qa, qb, begin, sorted_counts[j], single ? 1u : 0u, 0, 0};
-  const uint32_t h = a.head_ids[hl];
-  const uint64_t* ra = a.words + (size_t(h) * a.nq_global + a.q_ids[qa]) * a.wpr;
-  const uint64_t* rb = a.words + (size_t(h) * a.nq_global + a.q_ids[qb]) * a.wpr;
+  if (lane == 0) {
+    if (quad)
+      items[j] = WorkItem{r.hl, r.q[0], r.q[1], begin, sorted_counts[j], r.pad, r.q[2], r.q[3]};
+    else
+      items[j] = WorkItem{r.hl, r.q[0], a.step == 2 ? r.q[1] : r.q[0], begin, sorted_counts[j],
+                          (a.step == 1 || r.pad) ? 1u : 0u, 0, 0};
+  }
+  const uint32_t valid_shift = quad ? dbsp_core::kQuadValidShift : dbsp_core::kEntryValidShift;
   uint32_t out = begin;
   for (uint32_t w = 0; w < a.wpr; ++w) {
-    const uint64_t wa = ra[w], wb = single ? 0ull : rb[w];
-    const uint64_t uni = (wa | wb) & a.present[w];
+    uint64_t rw[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) rw[q] = row_word(r, q, w);
+    const uint64_t uni = (rw[0] | rw[1] | rw[2] | rw[3]) & a.present[w];
     // lanes take bits lane and lane+32 of the word, in ascending k order
     for (uint32_t half = 0; half < 2; ++half) {
       const uint32_t bit = half * 32 + lane;
@@ -98,14 +145,27 @@ __global__ void k2_write(K2Args a, uint32_t n_items, const unsigned long long* s
           const uint64_t rest = a.kv_tokens_global - start;
           valid = start >= a.kv_tokens_global ? 1u : uint32_t(rest < 64 ? rest : 64);
         }
-        const uint32_t e = uint32_t(a.kv_local[k]) | (((wa >> bit) & 1ull) ? dbsp_core::kEntryDenseA : 0u) |
-                           (((wb >> bit) & 1ull) ? dbsp_core::kEntryDenseB : 0u) |
-                           ((valid - 1) << dbsp_core::kEntryValidShift);
+        uint32_t e = uint32_t(a.kv_local[k]) | ((valid - 1) << valid_shift);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          if ((rw[q] >> bit) & 1ull) e |= 1u << (22 + q);  // pair: bits 22/23 = kEntryDenseA/B
         entries[out + __popc(mask & ((1u << lane) - 1u))] = e;
       }
       out += __popc(mask);
     }
   }
+}
+
+// DBSP_SCHED_AUTO_D128 on the device, the host rule of schedule.cpp in the
+// same double expressions: the CTA-pair (quad) list when its dense fraction
+// is at least kAutoQuadRatio of the pair list's.  gate = 1 selects the
+// CTA-pair kernel, 0 the pair-item kernel (both are launched; the other
+// returns at its first instruction).
+__global__ void k2_choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad,
+                          uint32_t* gate) {
+  const double f_pair = tot_pair[0] ? double(tot_pair[1]) / (2.0 * double(tot_pair[0])) : 1.0;
+  const double f_quad = tot_quad[0] ? double(tot_quad[1]) / (4.0 * double(tot_quad[0])) : 1.0;
+  *gate = f_quad >= dbsp_core::kAutoQuadRatio * f_pair ? 1u : 0u;
 }
 
 }  // namespace dbsp_dev
@@ -120,24 +180,19 @@ void ck(cudaError_t e, const char* what) {
 
 }  // namespace
 
-// Device-side state attached to a dbsp_schedule (see attention.cu).
-struct dbsp_device_schedule {
-  void* scratch = nullptr;
-  size_t scratch_bytes = 0;
-};
-
 namespace dbsp_k2 {
 
-// Builds into `items_out` / `entries_out` (device, caller-sized: n_items and
-// n_items * min(nk_local_present, nk) entries).  All work is stream-ordered.
+// Builds one layout into `items_out` / `entries_out` (device, caller-sized:
+// n_items and n_items * nk_local entries).  `totals` (2 x u64, zeroed here)
+// receives the tile visits and dense tiles when not null.  Stream-ordered.
 void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, const LocalView& v,
            uint32_t flags, const uint32_t* d_head_ids, const uint32_t* d_q_ids,
            const uint64_t* d_present, const int32_t* d_kv_local, dbsp_core::WorkItem* items_out,
-           uint32_t* entries_out, void*& scratch, size_t& scratch_bytes, cudaStream_t stream) {
-  const bool pair = (flags & kSchedPairQ) != 0;
+           uint32_t* entries_out, unsigned long long* totals, void*& scratch, size_t& scratch_bytes,
+           cudaStream_t stream) {
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
   if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder))) global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
-  const uint32_t step = pair ? 2 : 1;
+  const uint32_t step = (flags & kSchedQuad) ? 4 : (flags & kSchedPairQ) ? 2 : 1;
   const uint32_t per_head = (v.q_blocks + step - 1) / step;
   const uint32_t n = v.heads * per_head;
   if (n >= (1u << 24)) fail(kConfig, "too many work items for the device schedule builder");
@@ -153,7 +208,10 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   auto up = [&](size_t x) { return (x + al - 1) / al * al; };
   const size_t need = up(n * 4) + 2 * up(n * 8) + 2 * up(n * 4) + up(std::max(sort_tmp, scan_tmp));
   if (scratch_bytes < need) {
-    if (scratch) cudaFree(scratch);
+    if (scratch) {
+      ck(cudaStreamSynchronize(stream), "k2 scratch regrow");  // the previous build may still use it
+      cudaFree(scratch);
+    }
     scratch = nullptr;
     ck(cudaMalloc(&scratch, need), "cudaMalloc k2 scratch");
     scratch_bytes = need;
@@ -170,7 +228,8 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   uint32_t* begins = reinterpret_cast<uint32_t*>(s);
   s += up(n * 4);
   void* tmp = s;
-  dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, counts, keys);
+  if (totals) ck(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), stream), "k2 totals");
+  dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, counts, keys, totals);
   ck(cudaGetLastError(), "k2_count");
   size_t t1 = sort_tmp;
   ck(cub::DeviceRadixSort::SortKeys(tmp, t1, keys, sorted, int(n), 0, 64, stream), "k2 sort");
@@ -181,6 +240,12 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   dbsp_dev::k2_write<<<(n + 7) / 8, 256, 0, stream>>>(a, n, sorted, scounts, begins, items_out,
                                                       entries_out);
   ck(cudaGetLastError(), "k2_write");
+}
+
+void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
+            cudaStream_t stream) {
+  dbsp_dev::k2_choose<<<1, 1, 0, stream>>>(tot_pair, tot_quad, gate);
+  ck(cudaGetLastError(), "k2_choose");
 }
 
 }  // namespace dbsp_k2

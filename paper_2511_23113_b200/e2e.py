@@ -78,7 +78,7 @@ class HostStreamingAttention:
             sc = self.scheds[c]
             with torch.cuda.stream(self.s_comp):
                 sc.build_device(words, masks.num_kv_blocks, head_ids=np.arange(h0, h1), kv_tokens_global=S,
-                                stream=self.s_comp)
+                                head_dim=d, stream=self.s_comp)
                 sc.launch(qv, kv, vv, ov, stream=self.s_comp)
             ev_c = torch.cuda.Event()
             ev_c.record(self.s_comp)

@@ -16,7 +16,7 @@ import oracle, paper_2511_23113_b200 as D
 from paper_2511_23113_b200.attention import AttentionSchedule, sparse_attention
 res = {}
 fl = int(os.environ.get("DBSP_SWEEP_FLAGS", "1"))
-flags_for = lambda d: fl if d == 128 else fl & ~32  # the split-softmax kernel is d=128 only
+flags_for = lambda d: fl if d == 128 else fl & ~(8 | 16 | 128)  # the CTA-pair kernel is d=128 only
 # parity (toy + d128 clustered) with the swept schedule flags
 for (H, S, d, pat, lo, hi, seed) in [(8, 4096, 64, "random", .5, .5, 1), (4, 2048, 128, "clustered", .1, .6, 3)]:
     nb = S // 64

@@ -1,6 +1,6 @@
-"""compute-sanitizer target for the opt-in K4 kernels: one small launch per
+"""compute-sanitizer target for the K4 kernels: one small launch per
 schedule-flag set given on the command line (GPU-box tool):
-    compute-sanitizer --tool memcheck python tests/memcheck_probe.py 217 57"""
+    compute-sanitizer --tool memcheck python tests/memcheck_probe.py 153 1"""
 import sys
 from pathlib import Path
 
@@ -10,9 +10,9 @@ import torch  # noqa: E402
 import paper_2511_23113_b200 as D  # noqa: E402
 from paper_2511_23113_b200.attention import AttentionSchedule  # noqa: E402
 
-for fl in [int(x) for x in sys.argv[1:]] or [217]:
+for fl in [int(x) for x in sys.argv[1:]] or [153]:
     for d in (64, 128):
-        if fl & 192 and d != 128:
+        if fl & 128 and d != 128:
             continue
         H, S = 3, 1000
         nb = -(-S // 64)

@@ -48,8 +48,6 @@ def main():
     torch.cuda.synchronize()
     tr = buf.view(B, T, E).cpu().numpy().astype(np.int64)
     fn(None)
-    if os.environ.get("DBSP_K4_PAIR") == "1":  # CTA-pair kernel: default-kernel event layout
-        sched_flags &= ~8
     if mma:
         names = ["Sfree", "QK_t+2_issued", "Pfull", "Vfull", "PV_issued", "Kfull_t+2"]
         for b in (0, 2):
