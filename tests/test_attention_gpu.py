@@ -167,7 +167,7 @@ def test_partitioned_execution_matches_one_shot(strategy):
 
 
 @pytest.mark.parametrize("flags", [1, 1 | 8 | 16 | 128, 1 | 256])
-@pytest.mark.parametrize("pattern", ["clustered", "random"])
+@pytest.mark.parametrize("pattern", ["clustered", "random", "dense"])
 @pytest.mark.parametrize("case", ["identity", "rank_view", "ragged"])
 def test_device_schedule_matches_host(case, pattern, flags):
     # K2 on the GPU builds exactly the host builder's list (items, order,
@@ -175,7 +175,10 @@ def test_device_schedule_matches_host(case, pattern, flags):
     # choice between them (clustered masks pick quads, random masks pairs).
     from paper_2511_23113_b200.sp import rank_layouts
     H, nb = 8, 96
-    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pattern, 0.1, 0.6, 1.0, 11))
+    if pattern == "dense":
+        masks = D.AttentionMaskSet.from_dense(np.ones((H, nb, nb), bool))
+    else:
+        masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pattern, 0.1, 0.6, 1.0, 11))
     words = torch.from_numpy(masks.words.view(np.int64)).cuda()
     kw = {}
     S = nb * 64
@@ -189,8 +192,8 @@ def test_device_schedule_matches_host(case, pattern, flags):
     host = AttentionSchedule().build(masks, kv_tokens_global=S, flags=flags, **kw)
     dev = AttentionSchedule().build_device(words, nb, kv_tokens_global=S, flags=flags, **kw)
     assert host.layout() == dev.layout()
-    if flags == 1 | 256 and case == "identity":
-        assert dev.layout()["kernel"] == ("cta_pair_split_kv" if pattern == "clustered" else "pair_items")
+    if flags == 1 | 256 and case == "identity" and pattern != "clustered":
+        assert dev.layout()["kernel"] == ("cta_pair_split_kv" if pattern == "dense" else "pair_items")
     hi, he = host.download()
     di, de = dev.download()
     assert np.array_equal(hi, di)
