@@ -320,6 +320,24 @@ inline MachineProfile load_profile(const std::filesystem::path& path) {
   }
   return profile_from_json(j, path.string());
 }
+
+// Reference latency.hpp:377-379: the JSON above, pretty-printed, written
+// atomically (a temp file in the same directory, then rename), io_error on
+// failure.
+inline void save_profile(const MachineProfile& profile, const std::filesystem::path& path) {
+  const std::string text = profile_to_json(profile).dump(2) + "\n";
+  std::filesystem::path tmp = path;
+  tmp += ".tmp";
+  {
+    std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
+    if (!f) throw io_error("cannot open '" + tmp.string() + "' for writing");
+    f.write(text.data(), std::streamsize(text.size()));
+    if (!f) throw io_error("write failed for '" + tmp.string() + "'");
+  }
+  std::error_code ec;
+  std::filesystem::rename(tmp, path, ec);
+  if (ec) throw io_error("cannot rename '" + tmp.string() + "' to '" + path.string() + "': " + ec.message());
+}
 #endif
 
 }  // namespace dbsp

@@ -7,6 +7,9 @@
 #include "dbsp/attention.hpp"  // SpContext / sparse_attention: compiled and linked, not run (no GPU)
 #include <algorithm>
 #include <cmath>
+#include <filesystem>
+#include <fstream>
+#include <unistd.h>
 #include <cstdio>
 #include <functional>
 #include <limits>
@@ -16,6 +19,7 @@
 
 #include "dbsp/latency.hpp"
 #include "dbsp/mask.hpp"
+#include "dbsp/mask_io.hpp"
 #include "dbsp/metrics.hpp"
 #include "dbsp/planner.hpp"
 #include "dbsp/selector.hpp"
@@ -246,6 +250,41 @@ int main() {
               }) &&
               throws<config_error>([&] { BlockMask(0, 3); });
     expect(ok, "errors map to the reference exception classes");
+  }
+  // mask_io.hpp (reference mask_io.hpp:131-207) and save_profile (latency.hpp:377-379).
+  {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / ("dbsp_api_test_" + std::to_string(::getpid()));
+    fs::create_directories(dir);
+    Rng rng(777);
+    const AttentionMaskSet set = bernoulli_set(rng, 3, 5, 70, 0.4);
+    save_mask_set(set, dir / "m.bin");
+    bool ok = load_mask_set(dir / "m.bin") == set;
+    // a JSON fixture sidecar: 2 heads x 1 row, 12 KV blocks (2 bytes per row)
+    {
+      std::ofstream f(dir / "side.json");
+      f << R"({"heads": 2, "q_blocks": 1, "kv_blocks": 12, "block_size": 64, "rows": ["0108", "ff0f"]})";
+    }
+    const AttentionMaskSet side = load_mask_set(dir / "side.json");
+    ok = ok && side.head(0).get(0, 0) && side.head(0).get(0, 11) && side.head(0).row_popcount(0) == 2 &&
+         side.head(1).row_popcount(0) == 12;
+    {
+      std::ofstream f(dir / "bad.bin", std::ios::binary);
+      f << "DBSPMSK2garbage";
+    }
+    ok = ok && throws<parse_error>([&] { load_mask_set(dir / "bad.bin"); }) &&
+         throws<io_error>([&] { load_mask_set(dir / "missing.bin"); });
+    const MachineProfile prof = node();
+    save_profile(prof, dir / "p.json");
+    const MachineProfile back = load_profile(dir / "p.json");
+    // the JSON stores samples and load_profile re-fits them (as the reference
+    // does): curves come back exactly, the dense least-squares fit to rounding
+    auto close = [](double a, double b) { return std::fabs(a - b) <= 1e-12 * std::max(1.0, std::fabs(b)); };
+    ok = ok && close(back.dense_attn_seconds, prof.dense_attn_seconds) && close(back.launch_seconds, prof.launch_seconds) &&
+         back.all2all.size() == prof.all2all.size() && back.p2p.size() == prof.p2p.size() &&
+         back.all2all_at(8, 1e6) == prof.all2all_at(8, 1e6) && back.p2p_at(2, 3e5) == prof.p2p_at(2, 3e5);
+    fs::remove_all(dir);
+    expect(ok, "mask_io round trip + JSON sidecar + parse/io errors; save_profile -> load_profile");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
