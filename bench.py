@@ -209,30 +209,48 @@ def run_single(args, wl):
     v = torch.randn(S, H, d, device=dev, dtype=torch.bfloat16, generator=g)
     out = torch.empty_like(q)
 
+    # Host-built schedule: stats / layout for the report, and the host cost.
     t0 = time.perf_counter()
-    sched = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
+    hsched = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
     build_ms = (time.perf_counter() - t0) * 1e3
-    stats = sched.stats()
-    lay = sched.layout()
-    sched.upload()
+    stats = hsched.stats()
+    lay = hsched.layout()
+    del hsched
+    # One step = one call with live masks: K2 builds the work list on the GPU
+    # from the device-resident mask words (both layouts + the device-side
+    # kernel choice), then K4.  Events bracket K2 and K4 separately.
+    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).to(dev)
+    sched = AttentionSchedule()
     stream = torch.cuda.current_stream(dev)
+
+    def step():
+        sched.build_device(words, masks.num_kv_blocks, kv_tokens_global=S, head_dim=d, stream=stream)
+        sched.launch(q, k, v, out, stream=stream)
     for _ in range(args.warmup):
-        sched.launch(q, k, v, out)
+        step()
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    from paper_2511_23113_b200 import _lib
+    n_launch0 = _lib.lib().dbsp_launch_count()
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
-        ev[0].record(stream)
         for i in range(args.steps):
-            sched.launch(q, k, v, out)
-            ev[i + 1].record(stream)
+            ev[i][0].record(stream)
+            sched.build_device(words, masks.num_kv_blocks, kv_tokens_global=S, head_dim=d, stream=stream)
+            ev[i][1].record(stream)
+            sched.launch(q, k, v, out, stream=stream)
+            ev[i][2].record(stream)
         torch.cuda.synchronize()
-    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    ms = ev[0].elapsed_time(ev[-1]) / args.steps
+    n_launches = _lib.lib().dbsp_launch_count() - n_launch0
+    ms = ev[0][0].elapsed_time(ev[-1][2]) / args.steps
+    per = [e[1].elapsed_time(e[2]) for e in ev]          # K4 (both gated launches)
+    k2 = [e[0].elapsed_time(e[1]) for e in ev]           # K2 device schedule build
+    k4_ms = statistics.mean(per)
+    device_build_ms = round(statistics.mean(k2), 4)
     kernel_mhz = kernel_clock_mhz(lambda: sched.launch(q, k, v, out))
     flops = wl.flops_per_block() * total
     pk = peaks()
-    achieved = flops / (ms * 1e-3) / 1e12
+    achieved = flops / (k4_ms * 1e-3) / 1e12
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk["bf16_tflops"],
                 "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_tflops"], 4),
                 "frac_of_sustained": round(achieved / pk["bf16_tflops_sustained"], 4)
@@ -241,14 +259,18 @@ def run_single(args, wl):
                 "algorithmic_flops_per_launch": flops,
                 "per_unit": f"4*64*64*{d} FLOP per dense 64x64 tile x {total} dense tiles",
                 "issued_tile_frac": round(stats["dense_tiles"] / (lay["q_blocks_per_item"] * stats["tile_visits"]), 4),
-                "kernel_ms_min": round(min(per), 4), "kernel_ms_median": round(statistics.median(per), 4)}
+                "kernel_ms_mean": round(k4_ms, 4), "kernel_ms_min": round(min(per), 4),
+                "kernel_ms_median": round(statistics.median(per), 4),
+                "kernel": lay["kernel"],
+                "timing": "CUDA events around each step's K4 launch on its stream; value (ms_per_step) "
+                          "also includes the per-step K2 device schedule build"}
     # Second ceiling: the softmax's exp2 on the MUFU pipe, 16 per clock per SM on B200
     # (tests/ex2h_bench.cu), at the clock measured inside the kernel.  At d=64 a 64x64
     # tile's 4096 exps take twice its tensor time, so d=64 layers are exp-bound.
     exps = total * 64 * 64
     mufu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * (kernel_mhz or 1965.0) * 1e6
-    roofline["softmax_exp2"] = {"per_launch": exps, "achieved_per_s": round(exps / (ms * 1e-3), 1),
-                                "peak_per_s": round(mufu_peak, 1), "frac": round(exps / (ms * 1e-3) / mufu_peak, 4),
+    roofline["softmax_exp2"] = {"per_launch": exps, "achieved_per_s": round(exps / (k4_ms * 1e-3), 1),
+                                "peak_per_s": round(mufu_peak, 1), "frac": round(exps / (k4_ms * 1e-3) / mufu_peak, 4),
                                 "peak_basis": "16 ex2/clk/SM x SMs x in-kernel SM clock; d=64 runs 2 of 8 exp pairs "
                                               "on the FMA pipe, so frac may exceed 1 there"}
 
@@ -276,10 +298,10 @@ def run_single(args, wl):
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {**wl.describe(), "parallelism": "single-gpu (U1R1)", "strategy": "U1R1",
-                   "l2": "inputs larger than L2 (Q/K/V 3 x %.0f MB bf16 vs 126 MB L2)" % (q.numel() * 2 / 1e6),
-                   "density": round(D.density(masks), 4), "dense_tiles": total,
-                   "schedule": {**stats, **lay, "host_build_ms": round(build_ms, 2)}},
+        "config": bench_config(wl, 1),
+        "details": {"strategy": "U1R1", "density": round(D.density(masks), 4), "dense_tiles": total,
+                    "schedule": {**stats, **lay, "host_build_ms": round(build_ms, 2),
+                                 "device_build_ms": device_build_ms}},
         "rho_s": 1.0,
         "roofline": roofline,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d + sched_bytes,
@@ -287,7 +309,10 @@ def run_single(args, wl):
                 "note": "public API HostStreamingAttention per step: pinned host q/k/v streamed H2D in "
                         f"{args.e2e_chunks} head chunks (cudaMemcpy2DAsync), mask words H2D, K2 list build + K4 "
                         "per chunk on the GPU, D2H of o -- copies overlap the kernel on 3 streams"},
-        "gpu_launches": args.steps,
+        "gpu_launches": n_launches,
+        "gpu_launches_note": "our kernels in the timed region (dbsp_launch_count): per step K2 "
+                             "(k2_count, k2_sorted_counts, k2_write per layout + k2_choose) and both "
+                             "gated K4 launches, one of which returns at once; CUB sort/scan not counted",
         "clocks": {**clk.summary(), "sm_mhz_in_kernel": kernel_mhz,
                    "note": "sm_mhz: nvidia-smi samples over the timed region; sm_mhz_in_kernel: "
                            "clock64 / %globaltimer of CTA 0 inside one more K4 launch right after it"},
@@ -383,40 +408,151 @@ def ncu_traffic(workload_name: str):
         return None
 
 
+# ----------------------------------------------------------------------------- shared config
+def bench_config(wl, n_gpus: int) -> dict:
+    """The `config` both arms print (the driver compares them key for key):
+    the workload and the GPU count, nothing arm-specific."""
+    mb = wl.tokens * wl.heads * wl.head_dim * 2 / 1e6
+    l2 = ("inputs larger than L2 (Q/K/V bf16 %d MB each vs 126 MB L2), no flush" % round(mb)) if 3 * mb > 126 else \
+        ("inputs fit in L2 (Q/K/V bf16 %.1f MB each), no flush: K/V re-reads hit L2 by design" % mb)
+    return {**wl.describe(), "parallelism": "single-gpu (U1R1)" if n_gpus == 1 else
+            f"sp{n_gpus}: per-call U x R selection, db-SP plan", "l2": l2}
+
+
 # ----------------------------------------------------------------------------- reference arm
+def reference_masks(wl, gpus: int):
+    """The workload's masks generated by the COMPILED REFERENCE
+    (oracle/_ref/ref_bench: generate_mask_set + save_mask_set, DBSPMSK1), read
+    with numpy; falls back to the pure-Python restatement oracle/planner_ref.py.
+    The product library is never loaded on this arm."""
+    import numpy as np
+
+    import oracle
+    tool = oracle.ref_tool("ref_bench")
+    prof = ROOT / "paper_2511_23113_b200" / "profiles" / "b200_nominal.json"
+    if tool.exists():
+        fd, path = tempfile.mkstemp(suffix=".dbspmsk")
+        os.close(fd)
+        try:
+            r = subprocess.run([str(tool), str(wl.heads), str(wl.blocks), str(wl.blocks), wl.pattern,
+                                str(wl.min_density), str(wl.max_density), str(wl.seed), str(max(gpus, 1)), "1",
+                                str(prof), path], capture_output=True, text=True, timeout=600)
+            if r.returncode == 0:
+                words, _ = oracle.load_mask_words(path)
+                return words, "oracle/_ref/ref_bench (compiled reference generate_mask_set + save_mask_set)"
+        finally:
+            os.unlink(path)
+    from oracle import planner_ref as R
+    m = R.generate_mask_set(wl.heads, wl.blocks, wl.blocks, wl.pattern, wl.min_density, wl.max_density, 1.0,
+                            wl.seed)
+    return np.ascontiguousarray(m, np.uint64), "oracle/planner_ref.py (pure-Python restatement)"
+
+
 def run_reference(args, wl, rank: int) -> dict | None:
-    """The reference's CPU path of this hot path on the host cores: the
-    reference has no attention numerics, so attention is the oracle port (C,
-    OpenMP, all cores) on a bounded sample per step; the planner is the
-    reference's own compiled code (oracle/_ref/ref_bench)."""
+    """The reference's CPU path of this hot path on the host cores, rank 0
+    only.  The reference has no attention numerics, so a
+    step is (i) the reference's own select() for N GPUs (compiled reference,
+    oracle/_ref/ref_bench, single thread as the reference runs it) on the
+    workload's masks, plus (ii) the fp32 attention oracle (C, OpenMP on every
+    host core) over a FIXED bounded sample of (head, Q-block) rows.  `value`
+    is the measured time of that step; the full-layer extrapolation of (ii)
+    is reported separately."""
     if rank != 0:
         return None
-    import paper_2511_23113_b200 as D
-    masks = D.generate_mask_set(wl.spec())
+    import numpy as np
+
+    import oracle
+    words, masks_from = reference_masks(wl, args.gpus)
+    H, S, d, nb = wl.heads, wl.tokens, wl.head_dim, wl.blocks
+    g = np.random.default_rng(1234)
+    q, k, v = (g.standard_normal((S, H, d), dtype=np.float32) for _ in range(3))
+    per_row = np.array([[int(np.unpackbits(words[h, b].view(np.uint8)).sum()) for b in range(nb)]
+                        for h in range(H)])
+    total_tiles = int(per_row.sum())
+    order = np.random.default_rng(7).permutation(H * nb)
+    # calibrate the fixed sample to about --ref-budget seconds per step
+    probe = np.array([(i // nb, i % nb) for i in order[:16]], np.int32)
+    t0 = time.perf_counter()
+    oracle.sparse_attention(q, k, v, words, nb, rows=probe)
+    t_probe = time.perf_counter() - t0
+    tiles_probe = max(int(per_row[probe[:, 0], probe[:, 1]].sum()), 1)
+    want_tiles = tiles_probe * args.ref_budget / max(t_probe, 1e-6)
+    cum = np.cumsum(per_row.reshape(-1)[order])
+    n_rows = int(min(len(order), max(16, np.searchsorted(cum, want_tiles) + 1)))
+    rows = np.array([(i // nb, i % nb) for i in order[:n_rows]], np.int32)
+    sample_tiles = int(per_row[rows[:, 0], rows[:, 1]].sum())
+
+    # (i) the reference planner, per call, on the same masks (N > 1 only: at
+    # N = 1 there is nothing to select)
+    planner_ms, rp = 0.0, None
+    if args.gpus > 1:
+        rp = reference_planner_baseline(wl, gpus=args.gpus, reps=max(args.steps, 1))
+        planner_ms = rp["select_ms"] if rp else 0.0
     vals = []
-    last = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_attention_baseline(wl, masks, budget_s=args.ref_budget, seed=100 + i)
+        t0 = time.perf_counter()
+        oracle.sparse_attention(q, k, v, words, nb, rows=rows)
+        ms = (time.perf_counter() - t0) * 1e3
         if i >= args.warmup:
-            vals.append(cb["value"])
-        last = cb
-    rp = reference_planner_baseline(wl, gpus=max(args.gpus, 1))
+            vals.append(ms + planner_ms)
     value = statistics.mean(vals)
-    planner_ms = rp["select_ms"] if (rp and args.gpus > 1) else 0.0
-    total = value / max(args.gpus, 1) + planner_ms if args.gpus > 1 else value
-    cb = {"value": round(total, 3), "unit": "ms", "cores": last["cores"], "kind": "port",
-          "sample": last["sample"] + ("; + reference select() (compiled reference, 1 thread) "
-                                      f"{planner_ms:.2f} ms/call, attention split ideally over {args.gpus} ranks"
-                                      if args.gpus > 1 else "")}
-    res = {"metric": METRIC, "value": cb["value"], "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": cb["value"], "higher_is_better": False,
+    attn_ms = value - planner_ms
+    sample = (f"{n_rows} of {H * nb} (head, Q-block) rows = {sample_tiles} of {total_tiles} dense tiles "
+              f"({100.0 * sample_tiles / total_tiles:.2f}%), the same rows every step; fp32 in / fp64 accumulate "
+              "oracle (oracle/attention_ref.c)" +
+              (f" + reference select() for {args.gpus} GPUs ({planner_ms:.2f} ms/call, 1 thread)" if args.gpus > 1
+               else ""))
+    cb = {"value": round(value, 3), "unit": "ms", "cores": oracle.num_threads(), "kind": "port", "sample": sample}
+    res = {"metric": METRIC, "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(value, 3), "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {**wl.describe(), "parallelism": "cpu"}, "impl": "reference",
-           "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "ms", "h2d_bytes_per_step": 0,
-                                       "d2h_bytes_per_step": 0}}
+           "config": bench_config(wl, args.gpus), "impl": "reference",
+           "cpu_baseline": cb,
+           "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "extrapolated_full_layer_ms": round(attn_ms * total_tiles / sample_tiles + planner_ms, 1),
+           "extrapolation": "attention sample time x (all dense tiles / sampled dense tiles) + select(); "
+                            "not measured, for scale only",
+           "masks_from": masks_from}
     if rp:
         res["reference_planner"] = rp
+    res["native_so_loaded"] = loaded_native_libs()
     return res
+
+
+def loaded_native_libs() -> list:
+    """In-tree shared objects mapped into this process (/proc/self/maps)."""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return []
+    out = sorted({ln.split()[-1] for ln in maps if ln.split() and ln.split()[-1].startswith(str(ROOT))
+                  and ".so" in ln.split()[-1]})
+    return [str(Path(p).relative_to(ROOT)) for p in out]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` without torchrun: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 (one process per GPU)."""
+    if not args.dry_run and args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    env = dict(os.environ, DBSP_BENCH_LAUNCHED="1")
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -428,6 +564,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--balance", default="dbsp", choices=["dbsp", "uniform"])
+    ap.add_argument("--executor", default="native", choices=["native", "python"],
+                    help="N>1: the C++ SP executor (default) or the Python one")
+    ap.add_argument("--planner", default="device", choices=["device", "host"],
+                    help="N>1: per-call select() on the GPU (default) or on the host")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="N>1 launcher/loop check on CPU (gloo, no attention compute); not a measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--ref-budget", type=float, default=4.0)
@@ -437,11 +579,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
 
     from paper_2511_23113_b200.workloads import WORKLOADS
     wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        # N ranks requested without a launcher: become the launcher
+        sys.exit(launch_ranks(args))
+    world = int(world_env or "1")
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch with --nproc-per-node {args.gpus}",
+              file=sys.stderr)
+        sys.exit(2)
 
     if args.impl == "reference":
         res = run_reference(args, wl, rank)
@@ -449,11 +601,13 @@ def main():
             print(json.dumps(res), flush=True)
         return
 
-    # DBSP_BENCH_SP=1 runs the N>1 leg on a 1-rank group (exercises the
-    # distributed executors on one GPU; not a bench line of record)
-    if world > 1 or os.environ.get("DBSP_BENCH_SP") == "1":
+    if world > 1:
         from paper_2511_23113_b200.sp_bench import run_distributed
         res = run_distributed(args, wl, rank, world)
+        if res is not None:
+            # the details of this arm's run leave `config`, which both arms share
+            res["details"] = {k: v for k, v in res["config"].items() if k not in wl.describe()}
+            res["config"] = bench_config(wl, world)
     else:
         res = run_single(args, wl)
     if rank == 0 and res is not None:

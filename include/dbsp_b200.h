@@ -412,6 +412,10 @@ int dbsp_attention_launch_scatter(dbsp_schedule* sched, const dbsp_attn_args* ar
 /* Convenience: build + launch for a whole single-GPU problem (identity view). */
 int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, void* stream);
 
+/* Kernel launches this library has issued so far in the process (every
+ * launch site of its own kernels; CUB's kernels inside K2 are not counted). */
+uint64_t dbsp_launch_count(void);
+
 /* Strided host<->device copy (cudaMemcpy2DAsync): moves a head slice of a
  * token-major [tokens, heads, d] tensor, so host-resident layers can stream
  * to the GPU in head chunks that overlap with K4 (see e2e.py). */
@@ -438,6 +442,20 @@ void dbsp_sp_context_destroy(dbsp_sp_context* ctx);
 int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strategy strategy,
                       const dbsp_plan* plan, const void* q_home, const void* k_home, const void* v_home,
                       void* o_home, uint32_t tokens, uint32_t head_dim, void* stream);
+/* Empty ring groups are allowed: that period exchanges and computes nothing
+ * (the accumulator is finalised if it was a rank's last period).
+ * Per-period K4 timing of the next calls (CUDA events on the compute stream),
+ * read back with dbsp_sp_period_ms (ms[p] for ring period p of the last call;
+ * synchronises on those events).                                            */
+int dbsp_sp_set_timing(dbsp_sp_context* ctx, int32_t on);
+int dbsp_sp_period_ms(dbsp_sp_context* ctx, float* ms, uint32_t cap, uint32_t* n_periods);
+/* Waits until the call's work on `stream` and on the context's communication
+ * stream has finished, polling ncclCommGetAsyncError.  An asynchronous NCCL
+ * error, or no completion within timeout_ms (0 = no limit), aborts the
+ * communicator (ncclCommAbort) and returns DBSP_ERR_CUDA; every later call on
+ * the context then fails with DBSP_ERR_CUDA.  dbsp_sp_attention also checks
+ * the communicator's asynchronous error state on entry.                     */
+int dbsp_sp_synchronize(dbsp_sp_context* ctx, void* stream, uint32_t timeout_ms);
 /* The same call for all G = x*y ranks on this one GPU, device copies as the
  * transport: *_homes[g] are rank g's home shards.  Tests the multi-rank
  * layouts, packing and ring rotation without a second GPU.                  */

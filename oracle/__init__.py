@@ -98,6 +98,21 @@ def sparse_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, words: np.ndar
     return out, lse
 
 
+def load_mask_words(path) -> tuple:
+    """DBSPMSK1 file (reference mask_io.hpp:17-28: 28-byte header, then
+    heads*q_blocks rows of ceil(kv_blocks/8) bytes, key k at byte k/8 bit k%8)
+    -> (words uint64 [H, Nq, ceil(Nk/64)] in the BlockMask row layout, Nk)."""
+    data = np.fromfile(str(path), np.uint8)
+    if data[:8].tobytes() != b"DBSPMSK1":
+        raise ValueError(f"{path}: not a DBSPMSK1 file")
+    H, nq, nk, _bs = (int(x) for x in data[12:28].view("<u4"))
+    rb, wpr = (nk + 7) // 8, (nk + 63) // 64
+    rows = data[28:28 + H * nq * rb].reshape(H * nq, rb)
+    padded = np.zeros((H * nq, wpr * 8), np.uint8)
+    padded[:, :rb] = rows
+    return padded.view("<u8").reshape(H, nq, wpr).astype(np.uint64), nk
+
+
 def ref_tool(name: str) -> Path:
     """Path of a compiled reference tool in oracle/_ref (built here, shipped
     to the GPU box with the snapshot)."""

@@ -3,14 +3,18 @@
 // as the reference CPU planner baseline (single thread, as the reference
 // library is: it parallelises only compare/sweep, simulator.hpp:320,388).
 //
-// usage: ref_bench H Nq Nk pattern dmin dmax seed gpus reps profile.json
+// usage: ref_bench H Nq Nk pattern dmin dmax seed gpus reps profile.json [masks.bin]
 // prints one JSON line: per-strategy plan_dual ms, select() ms per call, rho.
+// With masks.bin, the generated set is also written there by the reference's
+// own save_mask_set (DBSPMSK1): bench.py's reference arm takes its masks from
+// it, so that arm never loads the product library.
 #include <chrono>
 #include <cstdio>
 #include <string>
 
 #include "dbsp/latency.hpp"
 #include "dbsp/mask.hpp"
+#include "dbsp/mask_io.hpp"
 #include "dbsp/metrics.hpp"
 #include "dbsp/planner.hpp"
 #include "dbsp/selector.hpp"
@@ -35,6 +39,7 @@ int main(int argc, char** argv) {
   const int reps = std::stoi(argv[9]);
   const MachineProfile prof = load_profile(argv[10]);
   const AttentionMaskSet set = generate_mask_set(sp);
+  if (argc > 11) save_mask_set(set, argv[11]);
 
   std::string per = "{";
   bool first = true;

@@ -169,6 +169,9 @@ _SIGS = {
     "dbsp_sp_context_destroy": (None, [C.c_void_p]),
     "dbsp_sp_attention": (C.c_int, [C.c_void_p, P(MaskSetT), StrategyT, P(PlanT), C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, u32, u32, C.c_void_p]),
+    "dbsp_sp_set_timing": (C.c_int, [C.c_void_p, i32]),
+    "dbsp_sp_period_ms": (C.c_int, [C.c_void_p, P(C.c_float), u32, P(u32)]),
+    "dbsp_sp_synchronize": (C.c_int, [C.c_void_p, C.c_void_p, u32]),
     "dbsp_sp_attention_simulated": (C.c_int, [P(MaskSetT), StrategyT, P(PlanT), C.c_void_p, C.c_void_p,
                                               C.c_void_p, C.c_void_p, u32, u32, C.c_void_p]),
     "dbsp_schedule_create": (C.c_int, [P(C.c_void_p)]),
@@ -184,6 +187,7 @@ _SIGS = {
     "dbsp_attention_launch": (C.c_int, [C.c_void_p, P(AttnArgsT), C.c_void_p]),
     "dbsp_attention_launch_scatter": (C.c_int, [C.c_void_p, P(AttnArgsT), P(OutScatterT), C.c_void_p]),
     "dbsp_sparse_attention": (C.c_int, [P(MaskSetT), P(AttnArgsT), C.c_void_p]),
+    "dbsp_launch_count": (u64, []),
     "dbsp_accum_init": (C.c_int, [C.c_void_p, C.c_void_p, u32, u32, u32, C.c_void_p]),
     "dbsp_copy_2d": (C.c_int, [C.c_void_p, u64, C.c_void_p, u64, u64, u64, i32, C.c_void_p]),
     "dbsp_mask_stats_device": (C.c_int, [C.c_void_p, u32, u32, u32, C.c_void_p, C.c_void_p,

@@ -116,6 +116,7 @@ void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute");
+  dbsp_core::count_launch();
   dbsp_dev::sparse_attn_fwd_kernel<D><<<items, dbsp_dev::kThreads, C::kSmemBytes, stream>>>(q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd launch");
 }
@@ -133,6 +134,7 @@ void launch_pd3(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute(pd3)");
+  dbsp_core::count_launch();
   dbsp_dev::sparse_attn_fwd_pd3_kernel<0><<<2 * items, dbsp_dev::kThreadsPd3, C::kSmemBytes, stream>>>(
       q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3 launch");
@@ -164,6 +166,14 @@ struct dbsp_schedule {
   size_t quad_offset = 0, quad_item_bytes = 0;
   void* view_dev = nullptr;  // head ids, q ids, present bitmap, kv_local table, totals, gate
   size_t view_bytes = 0;
+  // Host image of the view tables last copied to view_dev: an unchanged view
+  // (the same layer every call) costs no copy; a changed one goes through a
+  // pinned staging buffer, so the host never blocks on a pageable copy.
+  std::vector<uint8_t> view_image;
+  void* view_pinned = nullptr;
+  size_t view_pinned_bytes = 0;
+  cudaEvent_t view_copied = nullptr;
+  bool view_pending = false;
   uint32_t* gate = nullptr;
   unsigned long long* totals = nullptr;  // [pair visits, pair dense, quad visits, quad dense]
   void* k2_scratch = nullptr;
@@ -180,6 +190,9 @@ struct dbsp_schedule {
     if (dev) cudaFree(dev);
     if (pinned) cudaFreeHost(pinned);
     if (uploaded) cudaEventDestroy(uploaded);
+    if (view_pending && view_copied) cudaEventSynchronize(view_copied);
+    if (view_copied) cudaEventDestroy(view_copied);
+    if (view_pinned) cudaFreeHost(view_pinned);
     if (view_dev) cudaFree(view_dev);
     if (k2_scratch) cudaFree(k2_scratch);
   }
@@ -333,24 +346,44 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
       sched->pending = false;
     }
     // view_dev: present | totals (4 x u64) | gate (u32, padded) | hid | qid | kvl
-    const size_t vb = present.size() * 8 + 32 + 16 + hid.size() * 4 + qid.size() * 4 + kvl.size() * 4 + 64;
+    const size_t off_tot = present.size() * 8, off_hid = off_tot + 48;
+    const size_t off_qid = off_hid + hid.size() * 4, off_kvl = off_qid + qid.size() * 4;
+    const size_t vb = off_kvl + kvl.size() * 4;
+    std::vector<uint8_t> image(vb, 0);
+    std::memcpy(image.data(), present.data(), present.size() * 8);
+    std::memcpy(image.data() + off_hid, hid.data(), hid.size() * 4);
+    std::memcpy(image.data() + off_qid, qid.data(), qid.size() * 4);
+    std::memcpy(image.data() + off_kvl, kvl.data(), kvl.size() * 4);
     if (sched->view_bytes < vb) {
       if (sched->view_dev) cudaFree(sched->view_dev);
       sched->view_dev = nullptr;
-      cuda_check(cudaMalloc(&sched->view_dev, vb), "cudaMalloc view");
-      sched->view_bytes = vb;
+      cuda_check(cudaMalloc(&sched->view_dev, vb + 64), "cudaMalloc view");
+      sched->view_bytes = vb + 64;
+      sched->view_image.clear();
+    }
+    if (image != sched->view_image) {
+      if (!sched->view_copied)
+        cuda_check(cudaEventCreateWithFlags(&sched->view_copied, cudaEventDisableTiming), "event");
+      if (sched->view_pending) cuda_check(cudaEventSynchronize(sched->view_copied), "view staging sync");
+      if (sched->view_pinned_bytes < vb) {
+        if (sched->view_pinned) cudaFreeHost(sched->view_pinned);
+        sched->view_pinned = nullptr;
+        cuda_check(cudaMallocHost(&sched->view_pinned, vb), "cudaMallocHost view");
+        sched->view_pinned_bytes = vb;
+      }
+      std::memcpy(sched->view_pinned, image.data(), vb);
+      cuda_check(cudaMemcpyAsync(sched->view_dev, sched->view_pinned, vb, cudaMemcpyHostToDevice, stream), "view");
+      cuda_check(cudaEventRecord(sched->view_copied, stream), "event record");
+      sched->view_pending = true;
+      sched->view_image = std::move(image);
     }
     uint8_t* vd = static_cast<uint8_t*>(sched->view_dev);
     uint64_t* d_present = reinterpret_cast<uint64_t*>(vd);  // 8-byte aligned first
-    sched->totals = reinterpret_cast<unsigned long long*>(vd + present.size() * 8);
-    sched->gate = reinterpret_cast<uint32_t*>(vd + present.size() * 8 + 32);
-    uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + present.size() * 8 + 48);
-    uint32_t* d_qid = d_hid + hid.size();
-    int32_t* d_kvl = reinterpret_cast<int32_t*>(d_qid + qid.size());
-    cuda_check(cudaMemcpyAsync(d_present, present.data(), present.size() * 8, cudaMemcpyHostToDevice, stream), "view");
-    cuda_check(cudaMemcpyAsync(d_hid, hid.data(), hid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
-    cuda_check(cudaMemcpyAsync(d_qid, qid.data(), qid.size() * 4, cudaMemcpyHostToDevice, stream), "view");
-    cuda_check(cudaMemcpyAsync(d_kvl, kvl.data(), kvl.size() * 4, cudaMemcpyHostToDevice, stream), "view");
+    sched->totals = reinterpret_cast<unsigned long long*>(vd + off_tot);
+    sched->gate = reinterpret_cast<uint32_t*>(vd + off_tot + 32);
+    uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + off_hid);
+    uint32_t* d_qid = reinterpret_cast<uint32_t*>(vd + off_qid);
+    int32_t* d_kvl = reinterpret_cast<int32_t*>(vd + off_kvl);
 
     const bool auto_d128 = (flags & kSchedAutoD128) != 0;
     const bool quad_only = (flags & kSchedQuad) != 0;
@@ -653,6 +686,8 @@ int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, 
   return dbsp_attention_launch(os.sched, args, stream);
 }
 
+uint64_t dbsp_launch_count(void) { return dbsp_core::g_launches.load(std::memory_order_relaxed); }
+
 // Debug hook (not in the public header): device buffer of 16 blocks x 256
 // tiles x 8 events u64 clock64 stamps, used by DBSP_TRACE builds.
 int dbsp_debug_set_trace(unsigned long long* dev) {
@@ -683,6 +718,7 @@ int dbsp_accum_init(float* o_accum, float* lse_accum, uint32_t q_tokens, uint32_
   return guard([&] {
     if (!o_accum || !lse_accum) fail(kContract, "null accumulators");
     const size_t n_o = size_t(q_tokens) * heads * head_dim, n_l = size_t(q_tokens) * heads;
+    dbsp_core::count_launch();
     dbsp_dev::accum_init_kernel<<<592, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
         o_accum, lse_accum, n_o, n_l);
     cuda_check(cudaGetLastError(), "accum_init launch");
@@ -702,12 +738,14 @@ int dbsp_mask_stats_device(const uint64_t* d_words, uint32_t heads, uint32_t nq,
     cuda_check(cudaMemsetAsync(d_row_weights, 0, sizeof(uint64_t) * nq, stream), "memset");
     cuda_check(cudaMemsetAsync(d_col_weights, 0, sizeof(uint64_t) * nk, stream), "memset");
     const uint32_t rows = heads * nq;
+    dbsp_core::count_launch();
     dbsp_dev::mask_rows_kernel<<<(rows + 255) / 256, 256, 0, stream>>>(
         d_words, heads, nq, wpr, reinterpret_cast<unsigned long long*>(d_head_counts),
         reinterpret_cast<unsigned long long*>(d_row_weights));
     cuda_check(cudaGetLastError(), "mask_rows launch");
     const uint32_t rpb = 256;
     dim3 grid(wpr, (rows + rpb - 1) / rpb);
+    dbsp_core::count_launch();
     dbsp_dev::mask_cols_kernel<<<grid, 64, 0, stream>>>(
         d_words, rows, nk, wpr, rpb, reinterpret_cast<unsigned long long*>(d_col_weights));
     cuda_check(cudaGetLastError(), "mask_cols launch");

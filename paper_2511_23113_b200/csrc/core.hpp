@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -21,6 +22,12 @@
 #include <vector>
 
 namespace dbsp_core {
+
+// Kernel launches issued by this library (dbsp_launch_count): every launch
+// site of our kernels bumps it (CUB's own kernels inside K2 are not counted).
+inline std::atomic<uint64_t> g_launches{0};
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 
 // Status codes shared with the C ABI (include/dbsp_b200.h).
 enum Code : int {

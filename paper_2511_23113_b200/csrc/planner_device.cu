@@ -109,9 +109,11 @@ MaskStats mask_stats(const uint64_t* d_words, uint32_t H, uint32_t nq, uint32_t 
   unsigned long long* d = static_cast<unsigned long long*>(g_stats.device(n * 8));
   check(cudaMemsetAsync(d, 0, n * 8, stream), "memset");
   const uint32_t rows = H * nq;
+  dbsp_core::count_launch();
   dbsp_dev::mask_rows_kernel<<<(rows + 255) / 256, 256, 0, stream>>>(d_words, H, nq, wpr, d, d + H);
   check(cudaGetLastError(), "mask_rows launch");
   const uint32_t rpb = 256;
+  dbsp_core::count_launch();
   dbsp_dev::mask_cols_kernel<<<dim3(wpr, (rows + rpb - 1) / rpb), 64, 0, stream>>>(d_words, rows, nk, wpr, rpb,
                                                                                    d + H + nq);
   check(cudaGetLastError(), "mask_cols launch");
@@ -187,6 +189,7 @@ std::vector<Table> workload_tables(const uint64_t* d_words, const MaskView& m, c
   const uint32_t rows = m.H * m.nq;
   uint32_t max_cnt = 0;
   for (const auto& j : dj) max_cnt = std::max(max_cnt, j.y * j.gpus);
+  dbsp_core::count_launch();
   dbsp_dev::workload_tables_kernel<<<dim3((rows + 255) / 256, uint32_t(dj.size())), 256, max_cnt * 8, stream>>>(
       d_words, m.H, m.nq, uint32_t(wpr), reinterpret_cast<const dbsp_dev::TableJobDev*>(d),
       reinterpret_cast<const uint32_t*>(d + b_jobs), reinterpret_cast<const uint64_t*>(d + b_jobs + b_assign), dc);

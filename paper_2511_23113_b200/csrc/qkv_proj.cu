@@ -402,6 +402,7 @@ int dbsp_qkv_project(const dbsp_qkv_args* a, const dbsp_qkv_scatter* sc, void* s
       });
       ck(attr2, "cudaFuncSetAttribute(qkv pair)");
       const dim3 grid(2 * ((a->tokens + 255) / 256) * uint32_t(N / 256));
+      dbsp_core::count_launch();
       dbsp_dev::qkv_proj_pair_kernel<<<grid, dbsp_dev::kQkvThreads, dbsp_dev::kQkvPSmem,
                                        reinterpret_cast<cudaStream_t>(stream)>>>(tx, tw, p);
       ck(cudaGetLastError(), "qkv_proj_pair launch");
@@ -416,6 +417,7 @@ int dbsp_qkv_project(const dbsp_qkv_args* a, const dbsp_qkv_scatter* sc, void* s
     });
     ck(attr, "cudaFuncSetAttribute(qkv)");
     const dim3 grid(((a->tokens + 127) / 128) * uint32_t(N / 256));
+    dbsp_core::count_launch();
     dbsp_dev::qkv_proj_kernel<<<grid, dbsp_dev::kQkvThreads, dbsp_dev::kQkvSmem,
                                 reinterpret_cast<cudaStream_t>(stream)>>>(tx, tw, p);
     ck(cudaGetLastError(), "qkv_proj launch");

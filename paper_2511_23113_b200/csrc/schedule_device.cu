@@ -229,14 +229,17 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   s += up(n * 4);
   void* tmp = s;
   if (totals) ck(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), stream), "k2 totals");
+  dbsp_core::count_launch();
   dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, counts, keys, totals);
   ck(cudaGetLastError(), "k2_count");
   size_t t1 = sort_tmp;
   ck(cub::DeviceRadixSort::SortKeys(tmp, t1, keys, sorted, int(n), 0, 64, stream), "k2 sort");
+  dbsp_core::count_launch();
   dbsp_dev::k2_sorted_counts<<<(n + 255) / 256, 256, 0, stream>>>(sorted, counts, n, scounts);
   ck(cudaGetLastError(), "k2_sorted_counts");
   size_t t2 = scan_tmp;
   ck(cub::DeviceScan::ExclusiveSum(tmp, t2, scounts, begins, int(n), stream), "k2 scan");
+  dbsp_core::count_launch();
   dbsp_dev::k2_write<<<(n + 7) / 8, 256, 0, stream>>>(a, n, sorted, scounts, begins, items_out,
                                                       entries_out);
   ck(cudaGetLastError(), "k2_write");
@@ -244,6 +247,7 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
 
 void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
             cudaStream_t stream) {
+  dbsp_core::count_launch();
   dbsp_dev::k2_choose<<<1, 1, 0, stream>>>(tot_pair, tot_quad, gate);
   ck(cudaGetLastError(), "k2_choose");
 }

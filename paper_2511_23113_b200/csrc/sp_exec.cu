@@ -22,11 +22,16 @@
 #include <nccl.h>
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
+
+#include <chrono>
+#include <thread>
 
 #include <algorithm>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -51,6 +56,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 const NcclApi& N() {
@@ -76,6 +83,8 @@ const NcclApi& N() {
     sym(api.GroupStart, "ncclGroupStart");
     sym(api.GroupEnd, "ncclGroupEnd");
     sym(api.GetErrorString, "ncclGetErrorString");
+    sym(api.CommGetAsyncError, "ncclCommGetAsyncError");
+    sym(api.CommAbort, "ncclCommAbort");
   });
   if (!err.empty()) dbsp_core::fail(dbsp_core::kCuda, err);
   return api;
@@ -112,9 +121,27 @@ __global__ void sp_scatter_kernel(const uint4* __restrict__ src, uint32_t H, uin
     out[(orow * H + heads[j]) * d16 + c] = src[i];
   }
 }
+// A ring whose final period holds an empty KV group launches no K4 there:
+// the merged fp32 accumulator (already normalised, see the K4 epilogue) is
+// written out as bf16 instead.
+__global__ void sp_finalize_kernel(const float4* __restrict__ acc, uint2* __restrict__ out, size_t n4) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
+    const float4 a = acc[i];
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a.x, a.y), hi = __floats2bfloat162_rn(a.z, a.w);
+    out[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
 }  // namespace dbsp_dev
 
 namespace {
+
+// NVTX ranges for nsys / ncu --nvtx (header-only NVTX v3; no-ops without a tool).
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
@@ -206,6 +233,7 @@ void launch_gather(const void* src, uint32_t H, uint32_t d, const DevList& block
   if (!nrows || !heads.n) return;
   const size_t total = size_t(nrows) * heads.n * (d / 8);
   const uint32_t grid = uint32_t(std::min<size_t>((total + 255) / 256, 148 * 16));
+  dbsp_core::count_launch();
   dbsp_dev::sp_gather_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(src), H, d / 8, blocks.p, lo, heads.p,
                                                   heads.n, nrows, static_cast<uint4*>(dst));
   ck(cudaGetLastError(), "sp_gather launch");
@@ -217,6 +245,7 @@ void launch_scatter(const void* src, uint32_t H, uint32_t d, const DevList& bloc
   if (!nrows || !heads.n) return;
   const size_t total = size_t(nrows) * heads.n * (d / 8);
   const uint32_t grid = uint32_t(std::min<size_t>((total + 255) / 256, 148 * 16));
+  dbsp_core::count_launch();
   dbsp_dev::sp_scatter_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(src), H, d / 8, blocks.p, lo, heads.p,
                                                    heads.n, nrows, static_cast<uint4*>(out));
   ck(cudaGetLastError(), "sp_scatter launch");
@@ -265,6 +294,7 @@ struct RankExec {
   DevBuf q_loc, kbuf[2], vbuf[2], o_loc, o_acc, lse_acc;
   std::vector<DevBuf> sendq, sendk, sendv, recvo;
   DevBuf sendo;
+  DevBuf words;  // the call's mask words on the device (K2 input)
   std::vector<dbsp_schedule*> sched;  // per ring group
   dbsp_mask_set set{};
 
@@ -321,10 +351,20 @@ struct RankExec {
       back_blocks[src].set(in_range(all[src].q_blocks, lo, hi), st);
       back_heads[src].set(all[src].heads, st);
     }
-    // per-group K4 schedules over this rank's local view
+    // per-group K4 schedules over this rank's local view, built on the GPU (K2)
+    // from the call's mask words: a new plan or new masks cost one 1.3 MB copy
+    // (Wan layer) and a few small kernels, no host pass over the masks
     for (dbsp_schedule* sc : sched)
       if (sc) dbsp_schedule_destroy(sc);
     sched.assign(me.y, nullptr);
+    const size_t wpr = (size_t(mset->num_kv_blocks) + 63) / 64, per_head = size_t(mset->num_q_blocks) * wpr;
+    uint64_t* dw = nullptr;
+    if (!me.heads.empty() && !me.q_blocks.empty()) {
+      dw = static_cast<uint64_t*>(words.get(per_head * H * 8));
+      for (uint32_t h = 0; h < H; ++h)
+        ck(cudaMemcpyAsync(dw + h * per_head, mset->heads[h], per_head * 8, cudaMemcpyHostToDevice, st),
+           "mask words h2d");
+    }
     if (!me.heads.empty() && !me.q_blocks.empty())
       for (uint32_t g = 0; g < me.y; ++g) {
         if (me.groups[g].empty()) continue;
@@ -337,8 +377,11 @@ struct RankExec {
         v.num_kv_blocks = uint32_t(me.groups[g].size());
         v.kv_block_ids = me.groups[g].data();
         v.kv_tokens_global = tokens;
-        // pair schedule, or for d=128 the CTA-pair kernel where it pays (DBSP_SCHED_AUTO_D128)
-        rc(dbsp_schedule_build(sched[g], &set, &v, d == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : 1u));
+        // pair schedule, or for d=128 the CTA-pair kernel where it pays (DBSP_SCHED_AUTO_D128,
+        // decided on the device)
+        rc(dbsp_schedule_build_device(sched[g], dw, H, mset->num_q_blocks, mset->num_kv_blocks, &v,
+                                      d == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : DBSP_SCHED_PAIR_Q,
+                                      st));
       }
     // buffers
     size_t max_g = 1;
@@ -398,9 +441,16 @@ struct RankExec {
     const uint32_t hl = uint32_t(me.heads.size());
     if (p == 0 && y > 1) rc(dbsp_accum_init(static_cast<float*>(o_acc.p), static_cast<float*>(lse_acc.p),
                                             uint32_t(nq_loc * 64), hl, d, st));
-    if (!sched[g]) {
-      if (y == 1) ck(cudaMemsetAsync(o_loc.p, 0, nq_loc * 64 * row_bytes, st), "memset o");
-      else if (p == y - 1) fail(kInternal, "final ring period without KV blocks: finalize needs a launch");
+    if (!sched[g]) {  // empty KV group (or no dense tile reachable): nothing to attend to
+      if (y == 1) {
+        ck(cudaMemsetAsync(o_loc.p, 0, nq_loc * 64 * row_bytes, st), "memset o");
+      } else if (p == y - 1) {
+        const size_t n4 = nq_loc * 64 * hl * d / 4;
+        dbsp_core::count_launch();
+        dbsp_dev::sp_finalize_kernel<<<uint32_t(std::min<size_t>((n4 + 255) / 256, 148 * 8)), 256, 0, st>>>(
+            static_cast<const float4*>(o_acc.p), static_cast<uint2*>(o_loc.p), n4);
+        ck(cudaGetLastError(), "sp_finalize launch");
+      }
       return;
     }
     dbsp_attn_args a;
@@ -435,21 +485,22 @@ struct RankExec {
   }
 };
 
-// A ring period whose group is empty for this rank but is the last one would
-// leave finalize undone; the planner never produces an empty final group for
-// y > 1 with a non-empty Q set unless a whole KV group is empty -- handled by
-// the caller (ContractError) for now.
-
 }  // namespace
 
 struct dbsp_sp_context {
   ncclComm_t comm = nullptr;
+  bool aborted = false;
   uint32_t rank = 0, world = 1;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_done = nullptr;
   std::unique_ptr<RankExec> ex;
+  // per-period K4 timing of the last call (dbsp_sp_set_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_k;  // 2 per period
+  uint32_t timed_periods = 0;
   ~dbsp_sp_context() {
-    if (comm) N().CommDestroy(comm);
+    for (cudaEvent_t e : ev_k) cudaEventDestroy(e);
+    if (comm && !aborted) N().CommDestroy(comm);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     for (cudaEvent_t e : ev_ready)
       if (e) cudaEventDestroy(e);
@@ -469,6 +520,18 @@ Plan plan_from(const dbsp_mask_set* set, const dbsp_plan* p) {
   return o;
 }
 
+// A failed or aborted communicator fails every later call loudly.
+void check_comm(dbsp_sp_context* ctx) {
+  if (ctx->aborted) fail(kCuda, "the NCCL communicator was aborted after an error or a timeout");
+  ncclResult_t r = ncclSuccess;
+  nck(N().CommGetAsyncError(ctx->comm, &r), "ncclCommGetAsyncError");
+  if (r != ncclSuccess && r != ncclInProgress) {
+    N().CommAbort(ctx->comm);
+    ctx->aborted = true;
+    fail(kCuda, std::string("NCCL asynchronous error, communicator aborted: ") + N().GetErrorString(r));
+  }
+}
+
 void check_call(const dbsp_mask_set* set, dbsp_strategy s, const Plan& p, uint32_t world, uint32_t tokens,
                 uint32_t head_dim) {
   if (!set) fail(kContract, "null mask set");
@@ -478,10 +541,9 @@ void check_call(const dbsp_mask_set* set, dbsp_strategy s, const Plan& p, uint32
   if (head_dim != 64 && head_dim != 128) fail(kConfig, "head_dim must be 64 or 128");
   MaskView m = make_view(set->heads, set->num_heads, set->num_q_blocks, set->num_kv_blocks, set->block_size);
   validate_plan(m, Strategy{s.ulysses, s.ring}, p.head.data(), p.q.data(), p.kv.data());
-  if (s.ring > 1)
-    for (uint32_t g = 0; g < s.ring; ++g)
-      if (std::find(p.kv.begin(), p.kv.end(), g) == p.kv.end())
-        fail(kContract, "every ring group needs at least one KV block");
+  // Empty ring groups are allowed (a plan may leave a ring rank without KV
+  // blocks): such a period exchanges nothing and launches nothing, and if it
+  // is a rank's last period the accumulator is finalised by sp_finalize_kernel.
 }
 
 }  // namespace
@@ -522,6 +584,8 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
   return guard([&] {
     if (!ctx) fail(kContract, "null context");
     if (!q_home || !k_home || !v_home || !o_home) fail(kContract, "null home buffer");
+    Nvtx r_call("dbsp.sp_attention");
+    check_comm(ctx);
     const Plan p = plan_from(set, plan);
     check_call(set, s, p, ctx->world, tokens, head_dim);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
@@ -531,11 +595,20 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
     // plan or the masks change (a static-mask layer reuses them every step).
     const uint64_t key = call_key(set, Strategy{s.ulysses, s.ring}, p, tokens, head_dim);
     if (key != E.key) {
+      Nvtx r_plan("dbsp.sp_plan");
       E.plan(set, Strategy{s.ulysses, s.ring}, p, ctx->world, ctx->rank, tokens, head_dim, st);
       E.key = key;
     }
     const uint32_t G = ctx->world, me = ctx->rank;
+    if (ctx->timing && ctx->ev_k.size() < 2 * size_t(s.ring)) {
+      const size_t old = ctx->ev_k.size();
+      ctx->ev_k.resize(2 * size_t(s.ring));
+      for (size_t i = old; i < ctx->ev_k.size(); ++i) ck(cudaEventCreate(&ctx->ev_k[i]), "timing event");
+    }
+    ctx->timed_periods = ctx->timing ? s.ring : 0;
     // 1. fused all-to-all(v) on the compute stream (it gates everything after it)
+    std::optional<Nvtx> r_fwd;
+    r_fwd.emplace("dbsp.a2av_forward");
     E.pack_forward(q_home, k_home, v_home, st);
     nck(N().GroupStart(), "group");
     for (uint32_t x = 0; x < G; ++x) {
@@ -564,12 +637,14 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
       }
     }
     nck(N().GroupEnd(), "group");
+    r_fwd.reset();
     // 2. ring periods: K4 on the held group while the next one arrives on the comm stream
     const Layout& L = E.me;
     const uint32_t y = L.y;
     const uint32_t nxt = L.u * y + (L.r + 1) % y, prv = L.u * y + (L.r + y - 1) % y;
     int cur = 0;
     for (uint32_t pd = 0; pd < y; ++pd) {
+      Nvtx r_period("dbsp.ring_period");
       if (pd + 1 < y) {
         const size_t n = L.groups[L.period_group(pd)].size() * 64 * E.row_bytes;
         const size_t nn = L.groups[L.period_group(pd + 1)].size() * 64 * E.row_bytes;
@@ -586,7 +661,12 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
         }
         nck(N().GroupEnd(), "group");
       }
-      E.compute(pd, cur, st);
+      if (ctx->timing) ck(cudaEventRecord(ctx->ev_k[2 * pd], st), "timing event");
+      {
+        Nvtx r_k4("dbsp.k4");
+        E.compute(pd, cur, st);
+      }
+      if (ctx->timing) ck(cudaEventRecord(ctx->ev_k[2 * pd + 1], st), "timing event");
       if (pd + 1 < y) {
         ck(cudaEventRecord(ctx->ev_done, ctx->comm_stream), "event");
         ck(cudaStreamWaitEvent(st, ctx->ev_done, 0), "wait");  // next group arrived, held one sent
@@ -594,6 +674,7 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
       cur = 1 - cur;
     }
     // 3. reverse all-to-all(v): O slices go home, then land in the home layout
+    Nvtx r_rev("dbsp.a2av_reverse");
     nck(N().GroupStart(), "group");
     for (uint32_t x = 0; x < G; ++x) {
       const size_t sb = size_t(E.oslice_n[x]) * 64 * E.row_bytes;
@@ -607,6 +688,49 @@ int dbsp_sp_attention(dbsp_sp_context* ctx, const dbsp_mask_set* set, dbsp_strat
     }
     nck(N().GroupEnd(), "group");
     E.unpack_reverse(o_home, st);
+  });
+}
+
+int dbsp_sp_set_timing(dbsp_sp_context* ctx, int32_t on) {
+  return guard([&] {
+    if (!ctx) fail(kContract, "null context");
+    ctx->timing = on != 0;
+  });
+}
+
+int dbsp_sp_period_ms(dbsp_sp_context* ctx, float* ms, uint32_t cap, uint32_t* n) {
+  return guard([&] {
+    if (!ctx || !n) fail(kContract, "null argument");
+    *n = ctx->timed_periods;
+    if (ctx->timed_periods > cap || (ctx->timed_periods && !ms)) fail(kContract, "period buffer too small");
+    for (uint32_t p = 0; p < ctx->timed_periods; ++p) {
+      ck(cudaEventSynchronize(ctx->ev_k[2 * p + 1]), "timing sync");
+      ck(cudaEventElapsedTime(&ms[p], ctx->ev_k[2 * p], ctx->ev_k[2 * p + 1]), "elapsed");
+    }
+  });
+}
+
+int dbsp_sp_synchronize(dbsp_sp_context* ctx, void* stream_ptr, uint32_t timeout_ms) {
+  return guard([&] {
+    if (!ctx) fail(kContract, "null context");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t a = cudaStreamQuery(st), b = cudaStreamQuery(ctx->comm_stream);
+      if (a == cudaSuccess && b == cudaSuccess) break;
+      if (a != cudaErrorNotReady && a != cudaSuccess) ck(a, "compute stream");
+      if (b != cudaErrorNotReady && b != cudaSuccess) ck(b, "communication stream");
+      check_comm(ctx);  // aborts the communicator on an asynchronous NCCL error
+      const auto el = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+      if (timeout_ms && el.count() > int64_t(timeout_ms)) {
+        N().CommAbort(ctx->comm);
+        ctx->aborted = true;
+        fail(kCuda, "sequence-parallel call did not finish within " + std::to_string(timeout_ms) +
+                        " ms; NCCL communicator aborted");
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    check_comm(ctx);
   });
 }
 

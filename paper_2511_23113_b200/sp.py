@@ -28,7 +28,9 @@ from typing import Callable, Dict, List, Optional, Sequence
 
 import numpy as np
 
-from .planner import AttentionMaskSet, ContractError, ParallelStrategy, PartitionPlan
+from . import planner as _P
+from .planner import (AttentionMaskSet, ConfigError, ContractError, MachineProfile, ParallelStrategy,
+                      PartitionPlan, PlannerConfig, SelectorState)
 
 
 def home_range(rank: int, world: int, nblocks: int):
@@ -272,8 +274,10 @@ class SPAttention:
             if len(self.me.kv_groups[self.me.period_groups[y - 1]]) == 0 and nq_loc and Hu:
                 qmap, _ = scatter_maps(self.me, world, self.nb, self.S)
                 hs = torch.as_tensor(self.me.heads, device=dev)
+                elem_off = int(self._symm.offset) // self._home_out.element_size()
                 for i, (r, row0, _n) in enumerate(qmap):
-                    peer = self._symm.get_buffer(int(r), tuple(self._home_out.shape), dt)
+                    # the same peer address the kernel stores to (buffer_ptrs + offset)
+                    peer = self._symm.get_buffer(int(r), tuple(self._home_out.shape), dt, storage_offset=elem_off)
                     peer[int(row0):int(row0) + 64, hs] = o_loc[i * 64:(i + 1) * 64]
             self._symm.barrier()
             res = self._home_out[:T_home]
@@ -559,6 +563,32 @@ class NativeSPContext:
                                         C.c_void_p(out_home.data_ptr()), S, d, C.c_void_p(st.cuda_stream)))
         return out_home
 
+    def set_timing(self, on: bool) -> None:
+        """Per-period K4 events on the compute stream for the next calls."""
+        from . import _lib as L
+        from .planner import check
+        check(L.lib().dbsp_sp_set_timing(self._h, int(on)))
+
+    def period_ms(self) -> List[float]:
+        """K4 milliseconds per ring period of the last timed call (syncs on its events)."""
+        import ctypes as C
+        from . import _lib as L
+        from .planner import check
+        buf = (C.c_float * 64)()
+        n = C.c_uint32()
+        check(L.lib().dbsp_sp_period_ms(self._h, buf, 64, C.byref(n)))
+        return [float(buf[i]) for i in range(n.value)]
+
+    def synchronize(self, stream=None, timeout_ms: int = 60000) -> None:
+        """Wait for the last call, polling NCCL's asynchronous error state; an
+        error or a timeout aborts the communicator and raises CudaError."""
+        import ctypes as C
+        import torch
+        from . import _lib as L
+        from .planner import check
+        st = stream if stream is not None else torch.cuda.current_stream()
+        check(L.lib().dbsp_sp_synchronize(self._h, C.c_void_p(st.cuda_stream), int(timeout_ms)))
+
 
 def native_sp_simulated(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan):
     """dbsp_sp_attention_simulated: all G ranks of the C++ executor on this GPU
@@ -578,3 +608,100 @@ def native_sp_simulated(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
                                               C.byref(plan.c()), arr(qs), arr(ks), arr(vs), arr(os_), S, d,
                                               C.c_void_p(torch.cuda.current_stream(q.device).cuda_stream)))
     return torch.cat(os_, 0)
+
+
+# ----------------------------------------------------------------------------- per-call runtime
+class SPLayerRunner:
+    """One attention layer per call under db-SP, the way the paper's runtime
+    runs it: every call, select() on the live masks picks
+    the U x R split and its dual-balanced plan (selector.hpp:55-75, per-layer
+    SelectorState with P_s head-plan reuse), then the SP executor runs it.
+
+    Planning is pipelined: prefetch(layer', masks') computes the selection for
+    the NEXT call right after this call's GPU work has been enqueued, so it
+    overlaps that work instead of sitting on the critical path.  With the GPU
+    selector (planner="device", dbsp_select_device) the mask integers run on a
+    separate planner stream and the host only waits for that stream; with
+    planner="host" the C++ selector runs on the host (the GIL is released in
+    the C call).  Every rank plans the same masks with the same state, so the
+    ranks agree without exchanging plans.
+
+    executor: "native" (C++/NCCL, csrc/sp_exec.cu) or "python" (SPAttention,
+    torch.distributed; takes attn_fn for CPU tests).  balance: "dbsp" runs the
+    selected plan, "uniform" the selected strategy's default plan (the USP
+    baseline)."""
+
+    def __init__(self, rank: int, world: int, profile: MachineProfile, *, config: Optional[PlannerConfig] = None,
+                 executor: str = "native", planner: str = "device", device=None,
+                 broadcast_id: Optional[Callable[[bytes], bytes]] = None, attn_fn: Optional[AttnFn] = None,
+                 group=None, balance: str = "dbsp", native_ctx: Optional["NativeSPContext"] = None):
+        if executor not in ("native", "python") or planner not in ("device", "host") or \
+                balance not in ("dbsp", "uniform"):
+            raise ConfigError("executor must be native|python, planner device|host, balance dbsp|uniform")
+        self.rank, self.world = rank, world
+        self.profile, self.config = profile, config or PlannerConfig()
+        self.state = SelectorState(world)
+        self.executor, self.planner, self.balance = executor, planner, balance
+        self.device, self.group, self.attn_fn = device, group, attn_fn
+        self._native = None
+        if executor == "native":
+            self._native = native_ctx or NativeSPContext(rank, world, broadcast_id)
+        self._py: Dict[tuple, SPAttention] = {}
+        self._next: Dict[int, object] = {}
+        self._plan_stream = None
+        if planner == "device":
+            import torch
+            self._plan_stream = torch.cuda.Stream(device)
+        self.calls = self.prefetched = 0
+        self.plan_host_ms: List[float] = []  # host time of every selection
+        self.exposed_host_ms = 0.0           # selections that ran inside a call (nothing prefetched)
+        self.last = None
+
+    def _select(self, layer: int, masks: AttentionMaskSet, words=None):
+        import time
+        t0 = time.perf_counter()
+        if self.planner == "device":
+            import torch
+            with torch.cuda.stream(self._plan_stream):
+                if words is None:
+                    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).to(
+                        self.device, non_blocking=False)
+                sel = _P.select_device(layer, words, masks.num_kv_blocks, self.profile, self.config, self.state,
+                                       stream=self._plan_stream)
+        else:
+            sel = _P.select(layer, masks, self.profile, self.config, self.state)
+        self.plan_host_ms.append((time.perf_counter() - t0) * 1e3)
+        return sel
+
+    def prefetch(self, layer: int, masks: AttentionMaskSet, words=None) -> None:
+        """Selection for the next call of `layer` (call right after __call__)."""
+        self._next[layer] = (self._select(layer, masks, words), masks)
+        self.prefetched += 1
+
+    def __call__(self, layer: int, masks: AttentionMaskSet, q_home, k_home, v_home, out_home=None,
+                 words=None, stream=None):
+        nxt = self._next.pop(layer, None)
+        if nxt is not None and nxt[1] is masks:
+            sel = nxt[0]
+        else:
+            sel = self._select(layer, masks, words)
+            self.exposed_host_ms += self.plan_host_ms[-1]
+        st = sel.strategy
+        plan = sel.outcome.plan if self.balance == "dbsp" else _P.default_plan(masks, st)
+        self.calls += 1
+        self.last = sel
+        if self._native is not None:
+            return self._native(masks, st, plan, q_home, k_home, v_home, out_home, stream=stream)
+        key = (str(st), self.balance, plan.head_assignment.tobytes(), plan.q_assignment.tobytes(),
+               plan.kv_assignment.tobytes(), id(masks))
+        sp = self._py.get(key)
+        if sp is None:
+            self._py.clear()
+            sp = SPAttention(masks, st, plan, masks.num_q_blocks * 64, q_home.shape[2], self.rank, self.world,
+                             self.device, attn_fn=self.attn_fn, group=self.group)
+            self._py[key] = sp
+        return sp(q_home, k_home, v_home, out_home)
+
+    @property
+    def native(self) -> Optional[NativeSPContext]:
+        return self._native

@@ -416,6 +416,30 @@ def test_native_sp_executor_matches_python_executor(strategy, balanced):
     assert torch.equal(got, ref)
 
 
+@pytest.mark.parametrize("strategy,empty", [("U4R2", 1), ("U2R4", 3), ("U2R4", 0), ("U1R8", 7)])
+def test_sp_executors_with_an_empty_ring_group(strategy, empty):
+    # A plan whose KV group `empty` holds no block: that ring period exchanges
+    # and computes nothing, and a rank whose LAST period it is finalises its
+    # accumulator without a K4 launch.  C++ and Python executors agree bit for
+    # bit and match the one-GPU kernel to bf16 rounding.
+    from paper_2511_23113_b200.sp import native_sp_simulated, simulate_on_one_gpu
+    H, S, d = 8, 4096, 128
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 33))
+    st = D.parse_strategy(strategy)
+    plan = D.default_plan(masks, st)
+    kv = plan.kv_assignment.copy()
+    kv[kv == empty] = (empty + 1) % st.ring
+    plan = D.PartitionPlan(plan.head_assignment, plan.q_assignment, kv)
+    q, k, v = (t.cuda() for t in make_qkv(S, H, d, 34))
+    ref, _ = simulate_on_one_gpu(q, k, v, masks, st, plan, time_kernels=False)
+    got = native_sp_simulated(q, k, v, masks, st, plan)
+    one = sparse_attention(q, k, v, masks)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    assert float((got.float() - one.float()).abs().max()) <= 2e-2
+
+
 def test_native_sp_context_nccl_single_rank():
     # The NCCL-backed C++ context on a 1-rank communicator.
     from paper_2511_23113_b200.sp import NativeSPContext

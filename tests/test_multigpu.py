@@ -1,18 +1,40 @@
-"""Multi-GPU parity of the three sequence-parallel executors over NCCL: the
-Python executor (sp.SPAttention), the same with the O return fused into K4's
-epilogue (symmetric memory), and the C++ executor (dbsp_sp_attention).  Every
-rank computes its home shard; rank 0 compares the gathered result with the
-one-GPU kernel.  Skipped on boxes with fewer than two GPUs (this round's pool
-has one); run as part of `pytest -m gpu` where more are visible."""
+"""Multi-GPU parity of the sequence-parallel executors over NCCL, one process
+per GPU: the Python executor (sp.SPAttention), the same with the O return
+fused into K4's epilogue (symmetric memory), the C++ executor
+(dbsp_sp_attention) and the per-call runtime (sp.SPLayerRunner: select() on
+the masks, then the C++ executor).  World = the largest of 8/4/2 GPUs
+present; every U x R split of that world (at 8: U8R1, U4R2, U2R4, U1R8) under
+the uniform USP plan and the db-SP plan, plus a plan with an empty ring
+group.  Rank 0 gathers the home shards and checks them against the CPU
+oracle on sampled (head, Q-block) rows (north_star tolerance) and against
+the one-GPU kernel.  Then `bench.py --gpus N` runs end to end.
+
+Skipped below two GPUs (this round's pool has one GPU per box); the tests run
+as part of `pytest -m gpu` wherever more are visible."""
+import json
 import os
 import socket
+import subprocess
+import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                                 reason="needs >= 2 GPUs")]
+
+ROOT = Path(__file__).resolve().parents[1]
+H, S, DH = 16, 4096, 128
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+
+def _world() -> int:
+    n = torch.cuda.device_count()
+    return 8 if n >= 8 else 4 if n >= 4 else 2
 
 
 def _free_port():
@@ -23,71 +45,131 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, strategy, mode, result_q):
+def _cases(world):
+    import paper_2511_23113_b200 as D
+    out = [(str(st), bal) for st in D.enumerate_strategies(world) for bal in ("uniform", "dbsp")]
+    # a plan with an empty ring group: ring degree >= 2, every KV block in groups != 1
+    ring = [st for st in D.enumerate_strategies(world) if st.ring >= 2]
+    if ring:
+        out.append((str(ring[0]), "empty_group"))
+    return out
+
+
+def _plan(D, masks, st, bal):
+    if bal == "dbsp":
+        return D.plan_dual(masks, st).plan
+    plan = D.default_plan(masks, st)
+    if bal == "empty_group":
+        kv = plan.kv_assignment.copy()
+        kv[kv == 1] = 0
+        plan = D.PartitionPlan(plan.head_assignment, plan.q_assignment, kv)
+    return plan
+
+
+def _worker(rank, world, port, mode, result_q):
     import torch
     import torch.distributed as dist
 
     import paper_2511_23113_b200 as D
-    from paper_2511_23113_b200.attention import sparse_attention
-    from paper_2511_23113_b200.sp import NativeSPContext, SPAttention, home_range
+    from paper_2511_23113_b200.sp import NativeSPContext, SPAttention, SPLayerRunner, home_range
+    from paper_2511_23113_b200.sp_bench import load_profile
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
                             device_id=dev)
     try:
         dist.barrier()
-        H, S, d = 8, 4096, 128
         nb = S // 64
         masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.5, 1.0, 61))
-        st = D.parse_strategy(strategy)
-        plan = D.plan_dual(masks, st).plan
         g = torch.Generator().manual_seed(62)
-        q, k, v = (torch.randn(S, H, d, generator=g).to(torch.bfloat16) for _ in range(3))
+        q, k, v = (torch.randn(S, H, DH, generator=g).to(torch.bfloat16) for _ in range(3))
         lo, hi = home_range(rank, world, nb)
         qh, kh, vh = (t[lo * 64:hi * 64].contiguous().to(dev) for t in (q, k, v))
-        if mode == "native":
-            def bcast(b):
-                obj = [b]
-                dist.broadcast_object_list(obj, src=0)
-                return obj[0]
-            ctx = NativeSPContext(rank, world, bcast)
-            out = ctx(masks, st, plan, qh, kh, vh)
-        else:
-            sp = SPAttention(masks, st, plan, S, d, rank, world, dev, fuse_return=(mode == "fused"))
-            out = sp(qh, kh, vh)
-        torch.cuda.synchronize()
-        parts = [torch.empty((home_range(r, world, nb)[1] - home_range(r, world, nb)[0]) * 64, H, d,
-                             device=dev, dtype=torch.bfloat16) for r in range(world)]
-        dist.all_gather(parts, out.contiguous())
+
+        def bcast(b):
+            obj = [b]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+        native = NativeSPContext(rank, world, bcast) if mode in ("native", "runner") else None
+        results = {}
+        cases = _cases(world) if mode != "runner" else [("auto", "dbsp"), ("auto", "uniform")]
+        for st_name, bal in cases:
+            if mode == "runner":
+                run = SPLayerRunner(rank, world, load_profile("wan"), executor="native", planner="device",
+                                    device=dev, balance=bal, native_ctx=native)
+                for layer in range(3):  # per-call selection, the next one prefetched
+                    out = run(layer, masks, qh, kh, vh)
+                    run.prefetch(layer, masks)
+                st_name = str(run.last.strategy)
+            else:
+                st = D.parse_strategy(st_name)
+                plan = _plan(D, masks, st, bal)
+                if mode == "native":
+                    out = native(masks, st, plan, qh, kh, vh)
+                    native.synchronize(timeout_ms=120000)
+                else:
+                    out = SPAttention(masks, st, plan, S, DH, rank, world, dev, fuse_return=(mode == "fused"))(
+                        qh, kh, vh)
+            torch.cuda.synchronize()
+            parts = [torch.empty((home_range(r, world, nb)[1] - home_range(r, world, nb)[0]) * 64, H, DH,
+                                 device=dev, dtype=torch.bfloat16) for r in range(world)]
+            dist.all_gather(parts, out.contiguous())
+            if rank == 0:
+                results[f"{st_name}/{bal}"] = torch.cat(parts, 0).cpu()
         if rank == 0:
-            full = torch.cat(parts, 0)
-            ref = sparse_attention(q.to(dev), k.to(dev), v.to(dev), masks)
-            err = float((full.float() - ref.float()).abs().max())
-            result_q.put(err)
+            import oracle
+            from paper_2511_23113_b200.attention import sparse_attention
+            one = sparse_attention(q.to(dev), k.to(dev), v.to(dev), masks).cpu()
+            rng = np.random.default_rng(3)
+            rows = np.array([(h, b) for h in range(H) for b in rng.choice(nb, 6, replace=False)], np.int32)
+            ref, _ = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                             masks.words, nb, rows=rows)
+            tok = np.concatenate([np.arange(b * 64, b * 64 + 64) for _, b in rows])
+            hd = np.repeat(rows[:, 0], 64)
+            errs = {}
+            for name, full in results.items():
+                a = full.float().numpy()[tok, hd]
+                r = ref[tok, hd]
+                errs[name] = (float(np.abs(a - r).max()), float(np.linalg.norm(a - r) / np.linalg.norm(r)),
+                              float((full.float() - one.float()).abs().max()))
+            result_q.put(errs)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("mode", ["python", "fused", "native"])
+@pytest.mark.parametrize("mode", ["python", "fused", "native", "runner"])
 def test_sp_executors_over_nccl(mode):
     import torch.multiprocessing as mp
     here = Path(__file__).resolve().parent
-    # spawned ranks import this module and the package from the repo
+    # spawned ranks import this module, the package and the oracle from the repo
     os.environ["PYTHONPATH"] = os.pathsep.join([str(here.parent), str(here), os.environ.get("PYTHONPATH", "")])
-    world = 4 if torch.cuda.device_count() >= 4 else 2
-    strategies = ["U2R2", "U4R1", "U1R4"] if world == 4 else ["U2R1", "U1R2"]
+    world = _world()
     ctx = mp.get_context("spawn")
-    for strategy in strategies:
-        q = ctx.Queue()
-        port = _free_port()
-        procs = [ctx.Process(target=_worker, args=(r, world, port, strategy, mode, q)) for r in range(world)]
-        for p in procs:
-            p.start()
-        for p in procs:
-            p.join(timeout=300)
-            assert p.exitcode == 0, f"{mode} {strategy}: rank exited with {p.exitcode}"
-        err = q.get(timeout=10)
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    errs = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0, f"{mode}: rank exited with {p.exitcode}"
+    assert errs
+    for name, (mx, rel, vs_one) in errs.items():
+        assert mx <= MAX_ABS and rel <= REL_L2, f"{mode} {name}: max-abs {mx:.3e} rel-L2 {rel:.3e} vs oracle"
         # ring merges differ from the one-shot kernel by bf16 rounding only
-        assert err <= 2e-2, f"{mode} {strategy}: max-abs {err:.3e} vs one GPU"
+        assert vs_one <= 2e-2, f"{mode} {name}: max-abs {vs_one:.3e} vs one GPU"
+
+
+def test_bench_n_gpus_end_to_end():
+    world = _world()
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", str(world), "--workload", "cogvideox",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, timeout=1800, env=env,
+                       cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    j = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert j["n_gpus"] == world and j["value"] > 0 and j["planning"]["ranks_agree"]
+    import paper_2511_23113_b200 as D
+    assert set(j["splits"]) == {f"{s}/{b}" for s in D.enumerate_strategies(world) for b in ("uniform", "dbsp")}
+    assert all(v["rho_s_measured"] is not None for v in j["splits"].values())
