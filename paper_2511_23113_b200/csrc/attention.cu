@@ -124,18 +124,21 @@ void launch_kernel(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap
 // The CTA-pair split-KV kernel (attn_kernel_pd3.cuh): one cluster of two CTAs
 // per quad item.  No exp2 runs on the FMA pipe at d=128 (kPoly 0): 1 and 2 of
 // 8 pairs measured 6.11 and 6.37 ms against 6.12 ms on Wan (tests/ab_probe.py).
+#ifndef DBSP_PD3_POLY
+#define DBSP_PD3_POLY 0
+#endif
 void launch_pd3(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                 const dbsp_dev::AttnParams& prm, uint32_t items, cudaStream_t stream) {
   using C = dbsp_dev::Pd3Cfg;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3_kernel<0>,
+    attr_err = cudaFuncSetAttribute(dbsp_dev::sparse_attn_fwd_pd3_kernel<DBSP_PD3_POLY>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
   });
   cuda_check(attr_err, "cudaFuncSetAttribute(pd3)");
   dbsp_core::count_launch();
-  dbsp_dev::sparse_attn_fwd_pd3_kernel<0><<<2 * items, dbsp_dev::kThreadsPd3, C::kSmemBytes, stream>>>(
+  dbsp_dev::sparse_attn_fwd_pd3_kernel<DBSP_PD3_POLY><<<2 * items, dbsp_dev::kThreadsPd3, C::kSmemBytes, stream>>>(
       q, k, v, prm);
   cuda_check(cudaGetLastError(), "sparse_attn_fwd_pd3 launch");
 }

@@ -391,30 +391,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
         load_s(v);  // pass 2
         release_s();
         if (tr0) PD_TR(3, t >> 1);
+#ifdef DBSP_PD3_EARLY_PVWAIT
         wait_pv();
+#endif
+        // The exps run BEFORE the wait for PV(t-2): only the P store and the O
+        // rescale need it, so the wait overlaps the MUFU work instead of
+        // preceding it (P stays in registers, 32 packed words).
         const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
         float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int j = 16 * c + i;
-            const float2 x = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nm2);
-            float2 pp;
-            if ((j & 7) < kPoly) {
-              pp = exp2_poly3_pair(x);
-            } else {
-              pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-            }
-            acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
-            pk[i] = pack_bf16x2(pp.x, pp.y);
+        for (int j = 0; j < 32; ++j) {
+          const float2 x = __ffma2_rn(make_float2(v[2 * j], v[2 * j + 1]), sc2, nm2);
+          float2 pp;
+          if ((j & 7) < kPoly) {
+            pp = exp2_poly3_pair(x);
+          } else {
+            pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
           }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            *reinterpret_cast<uint4*>(prow + (((4 * c + u) ^ (row & 7)) << 4)) =
-                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          acc2[j & 1] = __fadd2_rn(acc2[j & 1], pp);
+          pk[j] = pack_bf16x2(pp.x, pp.y);
         }
+#ifndef DBSP_PD3_EARLY_PVWAIT
+        wait_pv();
+#endif
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(prow + ((u ^ (row & 7)) << 4)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
         l += a2.x + a2.y;
       } else {
