@@ -389,11 +389,73 @@ def sp_projection(q, k, v, masks, G: int = 8) -> dict:
                                    "rho_s_measured": round(measured_rho(t), 4),
                                    "rho_s_plan": round(D.imbalance_ratio(D.workload_table(masks, st, plan)), 4),
                                    "max_abs_vs_single_gpu": round(err, 5)}
+    planning = planning_on_critical_path(q, k, v, masks, G)
     best_uniform = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("uniform"))
     best_dbsp = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("dbsp"))
     return {"gpus_simulated": G, "splits": out, "best_uniform_ms": best_uniform, "best_dbsp_ms": best_dbsp,
             "speedup_dbsp_vs_best_uniform": round(best_uniform / best_dbsp, 4),
+            "planning_on_critical_path": planning,
             "note": "per-rank kernels measured on one B200; communication not included"}
+
+
+def planning_on_critical_path(q, k, v, masks, G: int = 8, calls: int = 20) -> dict:
+    """Per-call select() beside the G-GPU critical path, measured on this GPU:
+    the heaviest rank's K4 launches of the selected split's db-SP plan run
+    back to back (fixed plan), then with the GPU selector (dbsp_select_device,
+    G GPUs) planning the next call on a second stream while each call's
+    kernels run (the SPLayerRunner pipeline), then with the selection run
+    before each call (not overlapped).  exposed = per-call time minus fixed."""
+    import torch
+
+    import paper_2511_23113_b200 as D
+    from paper_2511_23113_b200.sp import rank_launcher, time_ranks_on_one_gpu
+    from paper_2511_23113_b200.sp_bench import load_profile
+    prof = load_profile("wan")
+    sel = D.select(0, masks, prof, D.PlannerConfig(), D.SelectorState(G))
+    st, plan = sel.strategy, sel.outcome.plan
+    t = time_ranks_on_one_gpu(q, k, v, masks, st, plan)
+    crit = max(range(G), key=lambda r: sum(t[p][r] for p in range(st.ring)))
+    launch = rank_launcher(q, k, v, masks, st, plan, crit)
+    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).to(q.device)
+    plan_stream = torch.cuda.Stream(q.device)
+    state = D.SelectorState(G)
+    comp = torch.cuda.current_stream(q.device)
+
+    def select_next(layer):
+        with torch.cuda.stream(plan_stream):
+            return D.select_device(layer, words, masks.num_kv_blocks, prof, D.PlannerConfig(), state,
+                                   stream=plan_stream)
+
+    def timed(mode: str) -> float:
+        for _ in range(3):
+            launch()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for i in range(calls):
+            if mode == "sequential":
+                select_next(i)
+            launch()
+            if mode == "overlapped":
+                select_next(i)  # the host waits for the planner stream only
+        e1.record(comp)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / calls
+
+    fixed = timed("fixed")
+    ovl = timed("overlapped")
+    seq = timed("sequential")
+    t0 = time.perf_counter()
+    for i in range(5):
+        select_next(i)
+    sel_ms = (time.perf_counter() - t0) / 5 * 1e3
+    return {"split": str(st), "critical_rank": crit, "rank_ms_fixed_plan": round(fixed, 4),
+            "ms_per_call_overlapped": round(ovl, 4), "ms_per_call_sequential": round(seq, 4),
+            "exposed_ms_overlapped": round(ovl - fixed, 4), "exposed_ms_sequential": round(seq - fixed, 4),
+            "select_device_ms": round(sel_ms, 4),
+            "exposed_frac_overlapped": round((ovl - fixed) / fixed, 4),
+            "note": "GPU selector for G GPUs planning the next call on a second stream while the heaviest "
+                    "rank's kernels run (PAPER.md:513-514: planning <= 5% of the call)"}
 
 
 def ncu_traffic(workload_name: str):

@@ -136,6 +136,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
   const uint32_t myq[2] = {rank ? it.pad0 : it.qa, rank ? it.pad1 : it.qb};  // quad rows 2r, 2r+1
   auto leader = [&](uint32_t local_bar) { return mapa_shared(local_bar, 0); };
   clock_probe_mark(p, 0);
+#ifdef DBSP_TRACE_CTA
+  const unsigned long long c_start = clock64();
+  if (threadIdx.x == 0 && rank == 0 && p.trace) p.trace[4 * (blockIdx.x >> 1)] = globaltimer_ns();
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -316,8 +320,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
       mbar_wait(bSfull(st), (t >> 1) & 1);
       tc_fence_after();
       if (lane == 0 && hf == 0 && lg == 0) PD_TRC(2 * st, t >> 1);
-      // DBSP_TRACE_FINE (warp 0): 0 start, 2 S loaded, 6 max exchanged, 3 exp start,
-      // 4 P stored, 5 before the P arrive, 1 after it
+      // DBSP_TRACE_FINE (warp 0): 0 start, 2 S loaded, 6 max exchanged, 3 S reloaded
+      // and released, 5 exps done, 4 P stored (after the PV(t-2) wait), 1 P arrived
       const bool tr0 = lane == 0 && warp == 0;
       if (tr0) PD_TR(0, t >> 1);
       const uint32_t valid = ((e >> dbsp_core::kQuadValidShift) & 63u) + 1u;
@@ -412,6 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
           acc2[j & 1] = __fadd2_rn(acc2[j & 1], pp);
           pk[j] = pack_bf16x2(pp.x, pp.y);
         }
+        if (tr0) PD_TR(5, t >> 1);
 #ifndef DBSP_PD3_EARLY_PVWAIT
         wait_pv();
 #endif
@@ -446,7 +451,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P (generic writes) -> tensor core
       tc_fence_before();
       __syncwarp();
-      if (tr0) PD_TR(5, t >> 1);
       if (lane == 0) {
         if (rank == 0)
           mbar_arrive(bPfull(st));
@@ -565,6 +569,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
   cluster_sync();  // the leader's MMAs wrote into this CTA's TMEM / read its smem
   tc_fence_after();
   clock_probe_mark(p, 1);
+#ifdef DBSP_TRACE_CTA
+  if (threadIdx.x == 0 && rank == 0 && p.trace) {
+    p.trace[4 * (blockIdx.x >> 1) + 1] = globaltimer_ns();
+    p.trace[4 * (blockIdx.x >> 1) + 2] = smid();
+    p.trace[4 * (blockIdx.x >> 1) + 3] = clock64() - c_start;
+  }
+#endif
   if (warp == 17) tmem_dealloc_pair(tmem, 512);
 }
 

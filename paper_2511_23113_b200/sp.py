@@ -507,6 +507,46 @@ def time_ranks_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelSt
     return times
 
 
+def rank_launcher(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
+                  rank: int, scratch=None):
+    """A callable that launches ONE rank's per-period K4 kernels of UxRy on
+    this GPU (the same launches as time_ranks_on_one_gpu: contiguous views of
+    the rank's local footprint), for measuring what runs beside that rank's
+    critical path -- e.g. the next call's planning."""
+    from .attention import AttentionSchedule, accum_init
+    S, H, d = q.shape
+    lay = rank_layouts(strategy, plan, masks.num_q_blocks, masks.num_kv_blocks)[rank]
+    y = strategy.ring
+    if scratch is None:
+        scratch = time_scratch(q, k, v)
+    qf, kf, vf, of, af, lf = scratch
+    hl, nq = len(lay.heads), len(lay.q_blocks)
+    sq = nq * 64
+    q_loc, o_loc = qf[:sq * hl * d].view(sq, hl, d), of[:sq * hl * d].view(sq, hl, d)
+    o_acc, l_acc = af[:sq * hl * d].view(sq, hl, d), lf[:sq * hl].view(hl, sq)
+    calls = []
+    for p in range(y):
+        kvb = lay.kv_groups[lay.period_groups[p]]
+        if len(kvb) == 0 or hl == 0 or nq == 0:
+            continue
+        sk = len(kvb) * 64
+        sc = AttentionSchedule().build(masks, head_ids=lay.heads, q_block_ids=lay.q_blocks, kv_block_ids=kvb,
+                                       kv_tokens_global=S, head_dim=d)
+        sc.upload()
+        calls.append((sc, kf[:sk * hl * d].view(sk, hl, d), vf[:sk * hl * d].view(sk, hl, d), p == y - 1))
+
+    def launch(stream=None):
+        if y > 1 and calls:
+            accum_init(o_acc, l_acc)
+        for sc, k_loc, v_loc, last in calls:
+            if y == 1:
+                sc.launch(q_loc, k_loc, v_loc, o_loc, stream=stream)
+            else:
+                sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=o_acc, lse_accum=l_acc, accumulate=True,
+                          finalize=last, stream=stream)
+    return launch
+
+
 def time_scratch(q, k, v):
     """Flat scratch buffers for time_ranks_on_one_gpu (values copied from q/k/v)."""
     import torch

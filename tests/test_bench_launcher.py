@@ -78,3 +78,19 @@ def test_reference_arm_under_torchrun_prints_on_rank0_only():
     j = _line(r.stdout)  # exactly one line
     assert j["n_gpus"] == 2 and "reference_planner" in j
     assert j["value"] >= j["reference_planner"]["select_ms"]  # not divided by N
+
+
+def test_measure_comm_dry_run(tmp_path):
+    # tests/measure_comm.py (the NCCL all-to-all / ring-step sweep of the B200
+    # MachineProfile) end to end on gloo: self-launch, groups per degree,
+    # fit_profile, a profile JSON the selector loads.
+    out = tmp_path / "prof.json"
+    r = subprocess.run([sys.executable, str(ROOT / "tests" / "measure_comm.py"), "--gpus", "4", "--dry-run",
+                        "--out", str(out)], capture_output=True, text=True, timeout=600, cwd=str(ROOT),
+                       env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE")})
+    assert r.returncode == 0, r.stderr[-3000:]
+    j = json.loads(out.read_text())
+    assert j["comm_source"] == "dry-run" and {e["degree"] for e in j["all2all"]} == {2, 4}
+    import paper_2511_23113_b200 as D
+    prof = D.MachineProfile.from_json(j)
+    assert prof.all2all_at(4, 1 << 20) > 0 and prof.p2p_at(2, 1 << 20) > 0

@@ -44,6 +44,8 @@ def main():
     dur = en - st
     wall = en.max()
     cnt = items[:, 4].astype(np.int64)
+    if sched_flags & 128:  # CTA-pair kernel: count in 128-key steps
+        cnt = (cnt + 1) // 2
     # concurrency over time
     grid = np.linspace(0, wall, 200)
     conc = [(np.sum((st <= x) & (en > x))) for x in grid]
@@ -52,7 +54,7 @@ def main():
     dec = np.array_split(order, 10)
     res = {
         "wall_us": wall / 1e3, "items": n, "sms": int(len(np.unique(sm))),
-        "sum_item_us_per_slot": float(dur.sum() / 1e3 / (2 * 148)),
+        "sum_item_us_per_slot": float(dur.sum() / 1e3 / (74 if sched_flags & 128 else 2 * 148)),
         "mean_concurrency": float(np.mean(conc)), "conc_profile": [int(c) for c in conc[::10]],
         "tail_us_last_10pct_items_start": float((wall - np.percentile(st, 90)) / 1e3),
         "ns_per_tile_by_count_decile": [[int(cnt[i].mean()), float(np.median(per_tile[i]))] for i in dec],

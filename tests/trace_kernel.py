@@ -98,7 +98,7 @@ def main():
 
 
 def fine_report(tr):
-    """Stage-0 softmax phases (DBSP_TRACE_FINE): start, S loaded, max, P halves stored, arrive."""
+    """Stage-0 softmax phases of the CTA-pair kernel (DBSP_TRACE_FINE, attn_kernel_pd3.cuh)."""
     stats = {}
     for b in range(tr.shape[0]):
         t = tr[b].astype(np.int64)
@@ -106,11 +106,11 @@ def fine_report(tr):
         if n < 8:
             continue
         t = t[2:n]
-        for key, arr in [("ld_S", t[:, 2] - t[:, 0]), ("max", t[:, 6] - t[:, 2]), ("exp_half0", t[:, 3] - t[:, 6]),
-                         ("exp_half1", t[:, 4] - t[:, 3]), ("st_wait_arrive", t[:, 1] - t[:, 4]),
+        for key, arr in [("ld_S", t[:, 2] - t[:, 0]), ("max_exchange", t[:, 6] - t[:, 2]),
+                         ("reload_release", t[:, 3] - t[:, 6]), ("exps", t[:, 5] - t[:, 3]),
+                         ("pvwait_store", t[:, 4] - t[:, 5]), ("rescale_fence_arrive", t[:, 1] - t[:, 4]),
                          ("total", t[:, 1] - t[:, 0]), ("P_to_PV0", t[:, 7] - t[:, 1]),
-                         ("wait_next_S", t[1:, 0] - t[:-1, 1]), ("st_wait", t[:, 5] - t[:, 4]),
-                         ("arrive", t[:, 1] - t[:, 5])]:
+                         ("wait_next_S", t[1:, 0] - t[:-1, 1]), ("period", np.diff(t[:, 0]))]:
             stats.setdefault(key, []).append(float(np.median(arr)))
         if b < 4:
             print(f"block {b}: " + json.dumps({k: v[-1] for k, v in stats.items()}))
