@@ -181,6 +181,9 @@ struct dbsp_schedule {
   unsigned long long* totals = nullptr;  // [pair visits, pair dense, quad visits, quad dense]
   void* k2_scratch = nullptr;
   size_t k2_scratch_bytes = 0;
+  void* k2_scratch_q = nullptr;  // the quad list's K2 scratch (both lists are built per AUTO call)
+  size_t k2_scratch_q_bytes = 0;
+  alignas(16) uint8_t k2_pending[2][kPendingBytes];  // deferred entry writes (pair, quad)
   // The last launch that reads `dev`: any rewrite of the list (upload, device
   // build) on another stream waits for it.
   cudaEvent_t last_use = nullptr;
@@ -198,6 +201,7 @@ struct dbsp_schedule {
     if (view_pinned) cudaFreeHost(view_pinned);
     if (view_dev) cudaFree(view_dev);
     if (k2_scratch) cudaFree(k2_scratch);
+    if (k2_scratch_q) cudaFree(k2_scratch_q);
   }
 };
 
@@ -206,7 +210,8 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global,
            const dbsp_core::LocalView& v, uint32_t flags, const uint32_t* d_head_ids,
            const uint32_t* d_q_ids, const uint64_t* d_present, const int32_t* d_kv_local,
            dbsp_core::WorkItem* items_out, uint32_t* entries_out, unsigned long long* totals,
-           void*& scratch, size_t& scratch_bytes, cudaStream_t stream);
+           void*& scratch, size_t& scratch_bytes, cudaStream_t stream, void* deferred_storage);
+void write_deferred(const void* deferred_storage, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream);
 void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
             cudaStream_t stream);
 }
@@ -408,16 +413,24 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
       sched->dev_bytes = bytes;
     }
     uint8_t* base = static_cast<uint8_t*>(sched->dev);
+    // AUTO: plan both lists, choose on the device, then write only the chosen
+    // list's entries (fused path: the writers are gated on the choice).
     if (n_pair)
       dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, pair_flags, d_hid, d_qid, d_present, d_kvl,
                      reinterpret_cast<WorkItem*>(base), reinterpret_cast<uint32_t*>(base + pair_item_bytes),
-                     auto_d128 ? sched->totals : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream);
+                     auto_d128 ? sched->totals : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream,
+                     auto_d128 ? sched->k2_pending[0] : nullptr);
     if (n_quad)
       dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, quad_flags, d_hid, d_qid, d_present, d_kvl,
                      reinterpret_cast<WorkItem*>(base + pair_bytes),
                      reinterpret_cast<uint32_t*>(base + pair_bytes + quad_item_bytes),
-                     auto_d128 ? sched->totals + 2 : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream);
-    if (auto_d128) dbsp_k2::choose(sched->totals, sched->totals + 2, sched->gate, stream);
+                     auto_d128 ? sched->totals + 2 : nullptr, sched->k2_scratch_q, sched->k2_scratch_q_bytes,
+                     stream, auto_d128 ? sched->k2_pending[1] : nullptr);
+    if (auto_d128) {
+      dbsp_k2::choose(sched->totals, sched->totals + 2, sched->gate, stream);
+      dbsp_k2::write_deferred(sched->k2_pending[0], sched->gate, 0, stream);
+      dbsp_k2::write_deferred(sched->k2_pending[1], sched->gate, 1, stream);
+    }
     // Bounds for the launch-time checks; the host copy of the list is empty.
     sched->host.items.clear();
     sched->host.entries.clear();

@@ -74,6 +74,10 @@ uint32_t normalize_sched_flags(uint32_t flags);
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
 constexpr uint32_t kQuadValidShift = 26;
 
+// Opaque storage for a device build whose entry write is deferred until the
+// device-side AUTO_D128 choice (schedule_device.cu PendingWrite).
+constexpr size_t kPendingBytes = 256;
+
 // Builds the work items in LPT launch order (see schedule.cpp).
 void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out);
 

@@ -9,6 +9,9 @@
 //   CUB radix sort of (head | ~count | index) keys -> LPT order
 //   CUB exclusive scan of the sorted counts -> entry offsets
 //   k2_write  one warp per item: WorkItem + entries (ballot-compacted bit walk)
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
@@ -85,7 +88,7 @@ __global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned 
     }
     counts[i] = c;
     const unsigned long long head_key = a.head_order ? (unsigned long long)r.hl : 0ull;
-    keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
+    if (keys) keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
   }
   if (totals) {
     // warp-aggregated: one atomic pair per warp
@@ -156,6 +159,103 @@ __global__ void k2_write(K2Args a, uint32_t n_items, const unsigned long long* s
   }
 }
 
+// Small lists (n <= kFusedItems, the common case: one rank's view, or a
+// whole layer of <= 16K items): after k2_count (all SMs), the LPT sort, the
+// scan and the item records run in ONE CTA.  Key = (head << 22) | (0x3FFFFF - count), sorted stably by a block
+// radix sort over the blocked arrangement (item i in thread i / kK2Items), so
+// ties keep ascending item order exactly as the host's stable_sort does.
+constexpr int kK2Threads = 1024, kK2Items = 16, kFusedItems = kK2Threads * kK2Items;
+using K2Sort = cub::BlockRadixSort<uint32_t, kK2Threads, kK2Items, uint32_t>;
+using K2Scan = cub::BlockScan<uint32_t, kK2Threads>;
+using K2Red = cub::BlockReduce<unsigned long long, kK2Threads>;
+union K2Smem {
+  typename K2Sort::TempStorage sort;
+  typename K2Scan::TempStorage scan;
+  typename K2Red::TempStorage red;
+};
+
+__global__ void __launch_bounds__(kK2Threads, 1)
+    k2_plan_fused(K2Args a, uint32_t n_items, uint32_t key_bits, const uint32_t* __restrict__ counts,
+                  WorkItem* items, uint32_t* sorted_idx, uint32_t* begins) {
+  extern __shared__ __align__(16) uint8_t k2_smem[];
+  K2Smem& sm = *reinterpret_cast<K2Smem*>(k2_smem);
+  uint32_t keys[kK2Items], idx[kK2Items];
+#pragma unroll
+  for (int s = 0; s < kK2Items; ++s) {
+    const uint32_t i = threadIdx.x * kK2Items + s;
+    idx[s] = i;
+    keys[s] = 0xFFFFFFFFu;  // padding sorts last
+    if (i < n_items) {
+      const uint32_t hl = i / a.items_per_head;
+      keys[s] = ((a.head_order ? hl : 0u) << 22) | (0x3FFFFFu - counts[i]);  // counts < 2^22
+    }
+  }
+  K2Sort(sm.sort).Sort(keys, idx, 0, int(key_bits));
+  __syncthreads();
+  uint32_t cnt[kK2Items], sum = 0;
+#pragma unroll
+  for (int s = 0; s < kK2Items; ++s) {
+    cnt[s] = keys[s] == 0xFFFFFFFFu ? 0u : 0x3FFFFFu - (keys[s] & 0x3FFFFFu);
+    sum += cnt[s];
+  }
+  uint32_t base = 0;
+  K2Scan(sm.scan).ExclusiveSum(sum, base);
+  const bool quad = a.step == 4;
+#pragma unroll
+  for (int s = 0; s < kK2Items; ++s) {
+    const uint32_t j = threadIdx.x * kK2Items + s;
+    if (j < n_items) {
+      const ItemRows r = item_rows(a, idx[s]);
+      items[j] = quad ? WorkItem{r.hl, r.q[0], r.q[1], base, cnt[s], r.pad, r.q[2], r.q[3]}
+                      : WorkItem{r.hl, r.q[0], a.step == 2 ? r.q[1] : r.q[0], base, cnt[s],
+                                 (a.step == 1 || r.pad) ? 1u : 0u, 0, 0};
+      sorted_idx[j] = idx[s];
+      begins[j] = base;
+    }
+    base += cnt[s];
+  }
+}
+
+// Entries of a fused-planned list: one warp per sorted item.  With `gate`, a
+// device-side AUTO_D128 build writes only the layout it chose.
+__global__ void k2_write_fused(K2Args a, uint32_t n_items, const uint32_t* sorted_idx, const uint32_t* begins,
+                               uint32_t* entries, const uint32_t* gate, uint32_t gate_value) {
+  if (gate && *gate != gate_value) return;
+  const uint32_t j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x & 31;
+  if (j >= n_items) return;
+  const ItemRows r = item_rows(a, sorted_idx[j]);
+  const uint32_t valid_shift = a.step == 4 ? dbsp_core::kQuadValidShift : dbsp_core::kEntryValidShift;
+  uint32_t out = begins[j];
+  for (uint32_t w = 0; w < a.wpr; ++w) {
+    uint64_t rw[4];
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) rw[q] = row_word(r, q, w);
+    const uint64_t uni = (rw[0] | rw[1] | rw[2] | rw[3]) & a.present[w];
+    if (!uni) continue;
+    for (uint32_t half = 0; half < 2; ++half) {
+      const uint32_t bit = half * 32 + lane;
+      const bool on = (uni >> bit) & 1ull;
+      const uint32_t mask = __ballot_sync(0xffffffffu, on);
+      if (on) {
+        const uint32_t k = w * 64 + bit;
+        uint32_t valid = 64;
+        if (a.kv_tokens_global) {
+          const uint64_t start = uint64_t(k) * 64;
+          const uint64_t rest = a.kv_tokens_global - start;
+          valid = start >= a.kv_tokens_global ? 1u : uint32_t(rest < 64 ? rest : 64);
+        }
+        uint32_t e = uint32_t(a.kv_local[k]) | ((valid - 1) << valid_shift);
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          if ((rw[q] >> bit) & 1ull) e |= 1u << (22 + q);
+        entries[out + __popc(mask & ((1u << lane) - 1u))] = e;
+      }
+      out += __popc(mask);
+    }
+  }
+}
+
 // DBSP_SCHED_AUTO_D128 on the device, the host rule of schedule.cpp in the
 // same double expressions: the CTA-pair (quad) list when its dense fraction
 // is at least kAutoQuadRatio of the pair list's.  gate = 1 selects the
@@ -182,6 +282,23 @@ void ck(cudaError_t e, const char* what) {
 
 namespace dbsp_k2 {
 
+// A fused-planned list whose entries are not written yet (n = 0: none).
+struct PendingWrite {
+  dbsp_dev::K2Args a;
+  uint32_t n = 0;
+  const uint32_t* sorted_idx = nullptr;
+  const uint32_t* begins = nullptr;
+  uint32_t* entries = nullptr;
+};
+
+void write_fused(const PendingWrite& w, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream) {
+  if (!w.n) return;
+  dbsp_core::count_launch();
+  dbsp_dev::k2_write_fused<<<(w.n + 7) / 8, 256, 0, stream>>>(w.a, w.n, w.sorted_idx, w.begins, w.entries, gate,
+                                                             gate_value);
+  ck(cudaGetLastError(), "k2_write_fused");
+}
+
 // Builds one layout into `items_out` / `entries_out` (device, caller-sized:
 // n_items and n_items * nk_local entries).  `totals` (2 x u64, zeroed here)
 // receives the tile visits and dense tiles when not null.  Stream-ordered.
@@ -189,7 +306,9 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
            uint32_t flags, const uint32_t* d_head_ids, const uint32_t* d_q_ids,
            const uint64_t* d_present, const int32_t* d_kv_local, dbsp_core::WorkItem* items_out,
            uint32_t* entries_out, unsigned long long* totals, void*& scratch, size_t& scratch_bytes,
-           cudaStream_t stream) {
+           cudaStream_t stream, void* deferred_storage) {
+  static_assert(sizeof(PendingWrite) <= kPendingBytes, "PendingWrite storage");
+  PendingWrite* deferred = static_cast<PendingWrite*>(deferred_storage);
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
   if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder))) global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
   const uint32_t step = (flags & kSchedQuad) ? 4 : (flags & kSchedPairQ) ? 2 : 1;
@@ -199,6 +318,46 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   dbsp_dev::K2Args a{d_words, nq_global, (nk_global + 63) / 64, d_head_ids, d_q_ids, v.q_blocks,
                      d_present, d_kv_local, v.kv_tokens_global, per_head, step,
                      global_lpt ? 0u : 1u};
+  const uint32_t head_bits = global_lpt ? 0u : uint32_t(32 - __builtin_clz(std::max(v.heads, 2u) - 1));
+  if (n <= uint32_t(dbsp_dev::kFusedItems) && 22 + head_bits <= 32) {
+    // one-CTA planner + a gated entry writer (5 launches for both AUTO layouts)
+    const size_t need = 3 * size_t(n) * 4 + 256;
+    if (scratch_bytes < need) {
+      if (scratch) {
+        ck(cudaStreamSynchronize(stream), "k2 scratch regrow");
+        cudaFree(scratch);
+      }
+      scratch = nullptr;
+      ck(cudaMalloc(&scratch, std::max<size_t>(need, 1 << 16)), "cudaMalloc k2 scratch");
+      scratch_bytes = std::max<size_t>(need, 1 << 16);
+    }
+    uint32_t* sidx = static_cast<uint32_t*>(scratch);
+    uint32_t* begins = sidx + n;
+    uint32_t* cnts = begins + n;
+    static std::once_flag attr;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr, [] {
+      attr_err = cudaFuncSetAttribute(dbsp_dev::k2_plan_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sizeof(dbsp_dev::K2Smem)));
+    });
+    ck(attr_err, "k2_plan_fused attribute");
+    if (totals) ck(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), stream), "k2 totals");
+    dbsp_core::count_launch();
+    dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, cnts, nullptr, totals);
+    ck(cudaGetLastError(), "k2_count");
+    dbsp_core::count_launch();
+    dbsp_dev::k2_plan_fused<<<1, dbsp_dev::kK2Threads, sizeof(dbsp_dev::K2Smem), stream>>>(
+        a, n, 22 + head_bits, cnts, items_out, sidx, begins);
+    ck(cudaGetLastError(), "k2_plan_fused");
+    PendingWrite w{a, n, sidx, begins, entries_out};
+    if (deferred) {
+      *deferred = w;  // written after the AUTO choice, gated
+    } else {
+      write_fused(w, nullptr, 0, stream);
+    }
+    return;
+  }
+  if (deferred) deferred->n = 0;  // the CUB path writes its entries itself
   // scratch: counts, keys, sorted keys, sorted counts, begins, cub temp
   size_t sort_tmp = 0, scan_tmp = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, (unsigned long long*)nullptr,
@@ -243,6 +402,10 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   dbsp_dev::k2_write<<<(n + 7) / 8, 256, 0, stream>>>(a, n, sorted, scounts, begins, items_out,
                                                       entries_out);
   ck(cudaGetLastError(), "k2_write");
+}
+
+void write_deferred(const void* deferred_storage, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream) {
+  write_fused(*static_cast<const PendingWrite*>(deferred_storage), gate, gate_value, stream);
 }
 
 void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
