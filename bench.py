@@ -405,6 +405,7 @@ def planning_on_critical_path(q, k, v, masks, G: int = 8, calls: int = 20) -> di
     G GPUs) planning the next call on a second stream while each call's
     kernels run (the SPLayerRunner pipeline), then with the selection run
     before each call (not overlapped).  exposed = per-call time minus fixed."""
+    import numpy as np
     import torch
 
     import paper_2511_23113_b200 as D
@@ -417,7 +418,7 @@ def planning_on_critical_path(q, k, v, masks, G: int = 8, calls: int = 20) -> di
     crit = max(range(G), key=lambda r: sum(t[p][r] for p in range(st.ring)))
     launch = rank_launcher(q, k, v, masks, st, plan, crit)
     words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).to(q.device)
-    plan_stream = torch.cuda.Stream(q.device)
+    plan_stream = torch.cuda.Stream(q.device, priority=-1)  # as SPLayerRunner's planner stream
     state = D.SelectorState(G)
     comp = torch.cuda.current_stream(q.device)
 

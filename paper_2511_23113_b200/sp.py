@@ -691,7 +691,9 @@ class SPLayerRunner:
         self._plan_stream = None
         if planner == "device":
             import torch
-            self._plan_stream = torch.cuda.Stream(device)
+            # high priority: the selector's small kernels take SMs at the next
+            # CTA boundary of the running attention instead of queueing behind it
+            self._plan_stream = torch.cuda.Stream(device, priority=-1)
         self.calls = self.prefetched = 0
         self.plan_host_ms: List[float] = []  # host time of every selection
         self.exposed_host_ms = 0.0           # selections that ran inside a call (nothing prefetched)

@@ -64,6 +64,8 @@ def main():
     A = np.vstack([cnt, np.ones_like(cnt)]).T.astype(np.float64)
     coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
     res["fixed_ns_fit"] = {"ns_per_tile": float(coef[0]), "ns_fixed": float(coef[1])}
+    cyc, *_ = np.linalg.lstsq(A, tr[:, 3].astype(np.float64), rcond=None)
+    res["fixed_cycles_fit"] = {"cycles_per_step": float(cyc[0]), "cycles_fixed": float(cyc[1])}
     print(json.dumps(res))
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    capture_output=True)
