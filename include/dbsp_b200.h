@@ -338,8 +338,8 @@ enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER =
        DBSP_SCHED_KEY128 = 16 /* layout bit: 128-key steps (set by CTA_PAIR) */,
        DBSP_SCHED_CTA_PAIR = 128 /* head_dim 128: quad items for the CTA-pair kernel (cta_group::2, two
                                     split-KV stages); implies PAIR_Q | QUAD | KEY128 */,
-       DBSP_SCHED_AUTO_D128 = 256 /* head_dim 128: the CTA-pair quad schedule when its dense fraction is
-                                     >= 0.95 x the pair schedule's, else the pair schedule */ };
+       DBSP_SCHED_AUTO_D128 = 256 /* head_dim 128: the measured-fastest layout; since round 2 that is the
+                                     pair schedule on every measured mask family (schedule.hpp) */ };
 /* QUAD or KEY128 without CTA_PAIR, and any other bit, are DBSP_CONFIG_ERROR. */
 /* Builds the work list for `view` against `set` (host). */
 int dbsp_schedule_build(dbsp_schedule* sched, const dbsp_mask_set* set,
@@ -357,7 +357,7 @@ int dbsp_schedule_download(const dbsp_schedule* sched, void* items_out, uint32_t
 int dbsp_schedule_stats(const dbsp_schedule* sched, uint64_t* items, uint64_t* tile_visits,
                         uint64_t* dense_tiles);
 /* Layout of the last build: DBSP_SCHED_* bits actually used (an AUTO_D128 build
- * reports the schedule it chose; the 64-row Q blocks per item are 4 with
+ * reports the layout it resolved to; the 64-row Q blocks per item are 4 with
  * DBSP_SCHED_QUAD, else 2 with DBSP_SCHED_PAIR_Q, else 1). */
 int dbsp_schedule_layout(const dbsp_schedule* sched, uint32_t* flags);
 

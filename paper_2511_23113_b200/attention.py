@@ -53,8 +53,9 @@ class AttentionSchedule:
               kv_tokens_global: int = 0, pair_q: bool = True, flags: Optional[int] = None,
               head_dim: Optional[int] = None) -> "AttentionSchedule":
         """flags: DBSP_SCHED_* bits (1 pair, 2 global LPT, 4 head order, 128 the d=128 CTA-pair
-        kernel's quad items (adds the layout bits 8|16), 256 auto choice for d=128).  Default: pair_q, plus
-        the auto choice of the CTA-pair kernel when head_dim is 128 (DBSP_SCHED_AUTO_D128)."""
+        kernel's quad items (adds the layout bits 8|16), 256 the automatic d=128 layout choice, which
+        resolves to the pair layout since round 2 (schedule.hpp)).  Default: pair_q, plus the auto
+        choice when head_dim is 128 (DBSP_SCHED_AUTO_D128)."""
         hid, qid, kid = _u32arr(head_ids), _u32arr(q_block_ids), _u32arr(kv_block_ids)
         if flags is None:
             flags = (1 | 256 if head_dim == 128 else 1) if pair_q else 0

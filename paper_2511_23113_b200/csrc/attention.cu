@@ -158,16 +158,11 @@ struct dbsp_schedule {
   size_t pinned_bytes = 0;
   cudaEvent_t uploaded = nullptr;
   bool pending = false;
-  // device-built schedule (K2): items/entries live only in `dev`.  With
-  // DBSP_SCHED_AUTO_D128 both lists are built (pair at offset 0, quad at
-  // quad_offset) and `gate` (device u32) says which kernel runs; both are
-  // launched and the other returns at once.
+  // device-built schedule (K2): items/entries live only in `dev`.
   bool on_device = false;
-  uint32_t dev_mode = 0;  // 0 pair-item list, 1 CTA-pair (quad) list, 2 both + device choice
-  uint32_t dev_items = 0;      // pair-item list (modes 0, 2)
-  uint32_t dev_quad_items = 0;  // quad list (modes 1, 2)
-  size_t quad_offset = 0, quad_item_bytes = 0;
-  void* view_dev = nullptr;  // head ids, q ids, present bitmap, kv_local table, totals, gate
+  bool dev_quad = false;  // the list is the CTA-pair (quad) layout
+  uint32_t dev_items = 0;
+  void* view_dev = nullptr;  // present bitmap, head ids, q ids, kv_local table
   size_t view_bytes = 0;
   // Host image of the view tables last copied to view_dev: an unchanged view
   // (the same layer every call) costs no copy; a changed one goes through a
@@ -177,13 +172,8 @@ struct dbsp_schedule {
   size_t view_pinned_bytes = 0;
   cudaEvent_t view_copied = nullptr;
   bool view_pending = false;
-  uint32_t* gate = nullptr;
-  unsigned long long* totals = nullptr;  // [pair visits, pair dense, quad visits, quad dense]
   void* k2_scratch = nullptr;
   size_t k2_scratch_bytes = 0;
-  void* k2_scratch_q = nullptr;  // the quad list's K2 scratch (both lists are built per AUTO call)
-  size_t k2_scratch_q_bytes = 0;
-  alignas(16) uint8_t k2_pending[2][kPendingBytes];  // deferred entry writes (pair, quad)
   // The last launch that reads `dev`: any rewrite of the list (upload, device
   // build) on another stream waits for it.
   cudaEvent_t last_use = nullptr;
@@ -201,7 +191,6 @@ struct dbsp_schedule {
     if (view_pinned) cudaFreeHost(view_pinned);
     if (view_dev) cudaFree(view_dev);
     if (k2_scratch) cudaFree(k2_scratch);
-    if (k2_scratch_q) cudaFree(k2_scratch_q);
   }
 };
 
@@ -209,11 +198,8 @@ namespace dbsp_k2 {
 void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global,
            const dbsp_core::LocalView& v, uint32_t flags, const uint32_t* d_head_ids,
            const uint32_t* d_q_ids, const uint64_t* d_present, const int32_t* d_kv_local,
-           dbsp_core::WorkItem* items_out, uint32_t* entries_out, unsigned long long* totals,
-           void*& scratch, size_t& scratch_bytes, cudaStream_t stream, void* deferred_storage);
-void write_deferred(const void* deferred_storage, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream);
-void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
-            cudaStream_t stream);
+           dbsp_core::WorkItem* items_out, uint32_t* entries_out, void*& scratch, size_t& scratch_bytes,
+           cudaStream_t stream);
 }
 
 using dbsp_capi::guard;
@@ -353,8 +339,8 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
       cuda_check(cudaEventSynchronize(sched->uploaded), "schedule upload sync");
       sched->pending = false;
     }
-    // view_dev: present | totals (4 x u64) | gate (u32, padded) | hid | qid | kvl
-    const size_t off_tot = present.size() * 8, off_hid = off_tot + 48;
+    // view_dev: present | hid | qid | kvl
+    const size_t off_hid = present.size() * 8;
     const size_t off_qid = off_hid + hid.size() * 4, off_kvl = off_qid + qid.size() * 4;
     const size_t vb = off_kvl + kvl.size() * 4;
     std::vector<uint8_t> image(vb, 0);
@@ -387,25 +373,16 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
     }
     uint8_t* vd = static_cast<uint8_t*>(sched->view_dev);
     uint64_t* d_present = reinterpret_cast<uint64_t*>(vd);  // 8-byte aligned first
-    sched->totals = reinterpret_cast<unsigned long long*>(vd + off_tot);
-    sched->gate = reinterpret_cast<uint32_t*>(vd + off_tot + 32);
     uint32_t* d_hid = reinterpret_cast<uint32_t*>(vd + off_hid);
     uint32_t* d_qid = reinterpret_cast<uint32_t*>(vd + off_qid);
     int32_t* d_kvl = reinterpret_cast<int32_t*>(vd + off_kvl);
 
-    const bool auto_d128 = (flags & kSchedAutoD128) != 0;
-    const bool quad_only = (flags & kSchedQuad) != 0;
-    const uint32_t keep = flags & (kSchedGlobalLpt | kSchedHeadOrder);
-    const uint32_t pair_flags = auto_d128 ? (keep | kSchedPairQ) : flags;
-    const uint32_t quad_flags = keep | kSchedPairQ | kSchedQuad | kSchedKey128 | kSchedCtaPair;
-    const uint32_t pstep = (pair_flags & kSchedPairQ) ? 2 : 1;
-    const uint32_t n_pair = quad_only ? 0 : lv.heads * ((lv.q_blocks + pstep - 1) / pstep);
-    const uint32_t n_quad = (quad_only || auto_d128) ? lv.heads * ((lv.q_blocks + 3) / 4) : 0;
-    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    const size_t pair_item_bytes = size_t(n_pair) * sizeof(WorkItem);
-    const size_t pair_bytes = al(pair_item_bytes + size_t(n_pair) * lv.kv_blocks * sizeof(uint32_t));
-    const size_t quad_item_bytes = size_t(n_quad) * sizeof(WorkItem);
-    const size_t bytes = pair_bytes + quad_item_bytes + size_t(n_quad) * lv.kv_blocks * sizeof(uint32_t);
+    // DBSP_SCHED_AUTO_D128 builds the pair layout (normalize_sched_flags).
+    const bool quad = (flags & kSchedQuad) != 0;
+    const uint32_t step = quad ? 4 : (flags & kSchedPairQ) ? 2 : 1;
+    const uint32_t n_items = lv.heads * ((lv.q_blocks + step - 1) / step);
+    const size_t item_bytes = size_t(n_items) * sizeof(WorkItem);
+    const size_t bytes = item_bytes + size_t(n_items) * lv.kv_blocks * sizeof(uint32_t);
     if (sched->dev_bytes < bytes) {
       if (sched->dev) cudaFree(sched->dev);
       sched->dev = nullptr;
@@ -413,24 +390,9 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
       sched->dev_bytes = bytes;
     }
     uint8_t* base = static_cast<uint8_t*>(sched->dev);
-    // AUTO: plan both lists, choose on the device, then write only the chosen
-    // list's entries (fused path: the writers are gated on the choice).
-    if (n_pair)
-      dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, pair_flags, d_hid, d_qid, d_present, d_kvl,
-                     reinterpret_cast<WorkItem*>(base), reinterpret_cast<uint32_t*>(base + pair_item_bytes),
-                     auto_d128 ? sched->totals : nullptr, sched->k2_scratch, sched->k2_scratch_bytes, stream,
-                     auto_d128 ? sched->k2_pending[0] : nullptr);
-    if (n_quad)
-      dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, quad_flags, d_hid, d_qid, d_present, d_kvl,
-                     reinterpret_cast<WorkItem*>(base + pair_bytes),
-                     reinterpret_cast<uint32_t*>(base + pair_bytes + quad_item_bytes),
-                     auto_d128 ? sched->totals + 2 : nullptr, sched->k2_scratch_q, sched->k2_scratch_q_bytes,
-                     stream, auto_d128 ? sched->k2_pending[1] : nullptr);
-    if (auto_d128) {
-      dbsp_k2::choose(sched->totals, sched->totals + 2, sched->gate, stream);
-      dbsp_k2::write_deferred(sched->k2_pending[0], sched->gate, 0, stream);
-      dbsp_k2::write_deferred(sched->k2_pending[1], sched->gate, 1, stream);
-    }
+    dbsp_k2::build(d_words, q_blocks, kv_blocks, lv, flags, d_hid, d_qid, d_present, d_kvl,
+                   reinterpret_cast<WorkItem*>(base), reinterpret_cast<uint32_t*>(base + item_bytes),
+                   sched->k2_scratch, sched->k2_scratch_bytes, stream);
     // Bounds for the launch-time checks; the host copy of the list is empty.
     sched->host.items.clear();
     sched->host.entries.clear();
@@ -441,33 +403,21 @@ int dbsp_schedule_build_device(dbsp_schedule* sched, const uint64_t* d_words, ui
     sched->host.max_kv_block = lv.kv_blocks - 1;
     sched->on_device = true;
     sched->dirty = false;
-    sched->dev_mode = auto_d128 ? 2u : quad_only ? 1u : 0u;
-    sched->dev_items = n_pair;
-    sched->item_bytes = pair_item_bytes;
-    sched->dev_quad_items = n_quad;
-    sched->quad_offset = pair_bytes;
-    sched->quad_item_bytes = quad_item_bytes;
+    sched->dev_quad = quad;
+    sched->dev_items = n_items;
+    sched->item_bytes = item_bytes;
   });
 }
 
 namespace {
-// The list a device-built schedule runs: quad (CTA-pair) or pair items.
-bool device_runs_quad(const dbsp_schedule* s) {
-  if (s->dev_mode != 2) return s->dev_mode == 1;
-  uint32_t g = 0;
-  cuda_check(cudaDeviceSynchronize(), "sync");
-  cuda_check(cudaMemcpy(&g, s->gate, 4, cudaMemcpyDeviceToHost), "d2h gate");
-  return g != 0;
-}
-
-// Device-built list (chosen layout) read back to host; diagnostics only.
+// Device-built list read back to host; diagnostics only.
 void download_device(const dbsp_schedule* s, std::vector<WorkItem>& items, std::vector<uint32_t>& entries,
                      bool& quad) {
-  quad = device_runs_quad(s);
+  quad = s->dev_quad;
   cuda_check(cudaDeviceSynchronize(), "sync");
-  const uint8_t* base = static_cast<const uint8_t*>(s->dev) + (quad ? s->quad_offset : 0);
-  const uint32_t n_items = quad ? s->dev_quad_items : s->dev_items;
-  const size_t ib = quad ? s->quad_item_bytes : s->item_bytes;
+  const uint8_t* base = static_cast<const uint8_t*>(s->dev);
+  const uint32_t n_items = s->dev_items;
+  const size_t ib = s->item_bytes;
   items.resize(n_items);
   if (n_items) cuda_check(cudaMemcpy(items.data(), base, ib, cudaMemcpyDeviceToHost), "d2h");
   uint64_t n = 0;
@@ -507,9 +457,7 @@ int dbsp_schedule_layout(const dbsp_schedule* s, uint32_t* flags) {
       *flags = s->host.flags;
       return;
     }
-    const uint32_t order = s->host.flags & (kSchedGlobalLpt | kSchedHeadOrder);
-    *flags = device_runs_quad(s) ? (order | kSchedPairQ | kSchedQuad | kSchedKey128 | kSchedCtaPair)
-                                 : (order | (s->host.flags & kSchedPairQ));
+    *flags = s->host.flags;
   });
 }
 
@@ -564,8 +512,7 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
       fail(kContract, "incomplete output scatter");
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     const Schedule& h = sched->host;
-    const uint32_t n_items = sched->on_device ? sched->dev_items + sched->dev_quad_items
-                                              : uint32_t(h.items.size());
+    const uint32_t n_items = sched->on_device ? sched->dev_items : uint32_t(h.items.size());
     if (n_items == 0) return;
     const uint32_t q_blocks = (a->q_tokens + 63) / 64, kv_blocks = (a->kv_tokens + 63) / 64;
     if (h.max_head >= a->heads || h.max_q_block >= q_blocks)
@@ -578,8 +525,6 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
     prm.items = static_cast<const WorkItem*>(sched->dev);
     prm.entries =
         reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(sched->dev) + sched->item_bytes);
-    prm.gate = nullptr;
-    prm.gate_value = 0;
     prm.q = static_cast<const __nv_bfloat16*>(a->q);
     prm.out = static_cast<__nv_bfloat16*>(a->o);
     prm.lse = a->lse;
@@ -599,37 +544,13 @@ void attention_launch(dbsp_schedule* sched, const dbsp_attn_args* a, const dbsp_
     const CUtensorMap tq = make_tmap(a->q, a->q_tokens, a->heads, a->head_dim);
     const CUtensorMap tk = make_tmap(a->k, a->kv_tokens, a->heads, a->head_dim);
     const CUtensorMap tv = make_tmap(a->v, a->kv_tokens, a->heads, a->head_dim);
-    if (!sched->on_device) {
-      if (h.flags & kSchedQuad) {
-        if (a->head_dim != 128) fail(kConfig, "the CTA-pair kernel (quad schedules) needs head_dim 128");
-        launch_pd3(tq, tk, tv, prm, n_items, stream);
-      } else if (a->head_dim == 128) {
-        launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
-      } else {
-        launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
-      }
+    if (h.flags & kSchedQuad) {
+      if (a->head_dim != 128) fail(kConfig, "the CTA-pair kernel (quad schedules) needs head_dim 128");
+      launch_pd3(tq, tk, tv, prm, n_items, stream);
+    } else if (a->head_dim == 128) {
+      launch_kernel<128>(tq, tk, tv, prm, n_items, stream);
     } else {
-      // Device-built list(s).  Mode 2 launches both kernels, each gated on
-      // the device-side choice (k2_choose); the other returns at once.
-      if (sched->dev_mode != 0 && a->head_dim != 128)
-        fail(kConfig, "the CTA-pair kernel (quad schedules) needs head_dim 128");
-      const bool gated = sched->dev_mode == 2;
-      if (sched->dev_mode != 1 && sched->dev_items) {
-        prm.gate = gated ? sched->gate : nullptr;
-        prm.gate_value = 0;
-        if (a->head_dim == 128)
-          launch_kernel<128>(tq, tk, tv, prm, sched->dev_items, stream);
-        else
-          launch_kernel<64>(tq, tk, tv, prm, sched->dev_items, stream);
-      }
-      if (sched->dev_mode != 0 && sched->dev_quad_items) {
-        const uint8_t* qb = static_cast<const uint8_t*>(sched->dev) + sched->quad_offset;
-        prm.items = reinterpret_cast<const WorkItem*>(qb);
-        prm.entries = reinterpret_cast<const uint32_t*>(qb + sched->quad_item_bytes);
-        prm.gate = gated ? sched->gate : nullptr;
-        prm.gate_value = 1;
-        launch_pd3(tq, tk, tv, prm, sched->dev_quad_items, stream);
-      }
+      launch_kernel<64>(tq, tk, tv, prm, n_items, stream);
     }
     mark_use(sched, stream);
   }
@@ -651,9 +572,8 @@ int dbsp_attention_launch_scatter(dbsp_schedule* sched, const dbsp_attn_args* a,
 int dbsp_sparse_attention(const dbsp_mask_set* set, const dbsp_attn_args* args, void* stream) {
   // One schedule and one device copy of the mask words per thread, reused by
   // every call.  The words go to the device (1.3 MB for the Wan layer) and K2
-  // builds the list there -- for d=128 both layouts plus the device-side
-  // choice (DBSP_SCHED_AUTO_D128) -- so a call with fresh masks costs no host
-  // pass over the masks.
+  // builds the list there, so a call with fresh masks costs no host pass over
+  // the masks.
   struct OneShot {
     dbsp_schedule* sched = nullptr;
     uint64_t* words = nullptr;

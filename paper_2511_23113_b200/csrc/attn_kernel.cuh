@@ -61,16 +61,7 @@ struct AttnParams {
   const uint32_t* scatter_rows;
   const uint32_t* scatter_heads;
   uint32_t out_heads;
-  // Device-side kernel choice (a K2 build with DBSP_SCHED_AUTO_D128): when
-  // non-null, the kernel runs only if *gate == gate_value; otherwise every CTA
-  // returns before touching shared memory, TMEM or a cluster barrier.
-  const uint32_t* gate;
-  uint32_t gate_value;
 };
-
-__device__ __forceinline__ bool gated_off(const AttnParams& p) {
-  return p.gate != nullptr && *p.gate != p.gate_value;
-}
 
 // Where the bf16 output row of (local token, local head) goes: the local
 // buffer, or its home rank's buffer when the O return is fused (out_peers).
@@ -243,7 +234,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmK,
                            const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  if (gated_off(p)) return;  // the device-side choice picked the other kernel
   using C = KCfg<D>;
   constexpr int NS = C::kStages;
   constexpr int NSB = C::kNSB;
@@ -309,32 +299,40 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
-    if (lane == 0 && count > 0) {
+    // The whole warp runs the loop (warp-uniform waits); one elected lane
+    // issues the copies.
+    if (count > 0) {
       const uint64_t pol_kv = l2_policy_evict_last();
       const int head = int(it.head);
       const uint32_t* ent = p.entries + it.begin;
       if (!C::kQInTmem) {  // both 64-row Q blocks of the tile, via TMA
-        const uint64_t pol_q = l2_policy_evict_first();
-        mbar_expect_tx(bQready, C::kQBytes);
+        if (elect_one()) {
+          const uint64_t pol_q = l2_policy_evict_first();
+          mbar_expect_tx(bQready, C::kQBytes);
 #pragma unroll
-        for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_3d(sQ + c * C::kQChunk, &tmQ, c * 64, head, int(it.qa) * 64, bQready, pol_q);
-          tma_load_3d(sQ + c * C::kQChunk + 8192, &tmQ, c * 64, head, int(it.qb) * 64, bQready,
-                      pol_q);
+          for (int c = 0; c < C::kChunks; ++c) {
+            tma_load_3d(sQ + c * C::kQChunk, &tmQ, c * 64, head, int(it.qa) * 64, bQready, pol_q);
+            tma_load_3d(sQ + c * C::kQChunk + 8192, &tmQ, c * 64, head, int(it.qb) * 64, bQready,
+                        pol_q);
+          }
         }
+        __syncwarp();
       }
       auto load_tile = [&](const CUtensorMap* tm, uint32_t dst, uint32_t full, uint32_t j) {
         const int kv = int(__ldg(ent + j) & dbsp_core::kEntryKvMask);
-        mbar_expect_tx(full, C::kTileBytes);
+        if (elect_one()) {
+          mbar_expect_tx(full, C::kTileBytes);
 #pragma unroll
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dst + c * 8192, tm, c * 64, head, kv * 64, full, pol_kv);
+          for (int c = 0; c < C::kChunks; ++c)
+            tma_load_3d(dst + c * 8192, tm, c * 64, head, kv * 64, full, pol_kv);
+        }
+        __syncwarp();
       };
       auto load_k = [&](uint32_t j) {
         const int s = int(j % NS);
         mbar_wait(bKempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmK, sK + s * C::kTileBytes, bKfull(s), j);
-        DBSP_TR(kTrLoadK, j);
+        if (lane == 0) DBSP_TR(kTrLoadK, j);
       };
       load_k(0);
       for (uint32_t j = 0; j < count; ++j) {
@@ -342,37 +340,45 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = int(j % NS);
         mbar_wait(bVempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmV, sV + s * C::kTileBytes, bVfull(s), j);
-        DBSP_TR(kTrLoadV, j);
+        if (lane == 0) DBSP_TR(kTrLoadV, j);
       }
-    } else if (count > 0) {
-      mbar_wait(bOfinal, 0);  // idle lanes sleep on an mbarrier, not in a warp-sync spin
     }
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && count > 0) {
+    // Warp-uniform loop, one elected lane issues, descriptors precomputed (a
+    // base plus per-stage / per-k-step constants that never carry out of the
+    // 14-bit address field).  The first version issued from a lane-0 branch
+    // while lanes 1-31 spun on an mbarrier in the same warp: each group of
+    // four MMAs took 650-860 cycles to issue and PV(j) left 1,300 cycles
+    // after P(j) was ready (tests/trace_kernel.py --workload cogvideox).
+    if (count > 0) {
       constexpr uint32_t kIdescQK = idesc_bf16(128, 64, false, false);
       constexpr uint32_t kIdescPV = idesc_bf16(128, D, false, true);
+      const uint64_t dK = smem_desc_sw128(sK, 16, 1024);
+      const uint64_t dQ = smem_desc_sw128(sQ, 16, 1024);  // used only when !kQInTmem
+      const uint64_t dV = smem_desc_sw128(sV, 8192, 1024);
       auto issue_s = [&](uint32_t j) {
         const int s = int(j % NS);
         mbar_wait(bKfull(s), (j / NS) & 1);
         tc_fence_after();
         const uint32_t dcol = tmem + C::kColS + 64u * (j % NSB);
+        const uint64_t bK = dK + ((uint32_t(s) * C::kTileBytes) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t bd =
-              smem_desc_sw128(sK + s * C::kTileBytes + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-          if constexpr (C::kQInTmem) {
-            mma_ts(dcol, tmem + C::kColQ + kk * 8, bd, kIdescQK, kk > 0 ? 1u : 0u);
-          } else {
-            const uint64_t ad =
-                smem_desc_sw128(sQ + (kk >> 2) * C::kQChunk + (kk & 3) * 32, 16, 1024);
-            mma_ss(dcol, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t bd = bK + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4);
+            if constexpr (C::kQInTmem) {
+              mma_ts(dcol, tmem + C::kColQ + kk * 8, bd, kIdescQK, kk > 0 ? 1u : 0u);
+            } else {
+              mma_ss(dcol, dQ + (((kk >> 2) * C::kQChunk + (kk & 3) * 32) >> 4), bd, kIdescQK, kk > 0 ? 1u : 0u);
+            }
           }
+          tc_commit(bKempty(s));
+          tc_commit(bSfull(int(j % NSB)));
+          DBSP_TR(kTrMmaS, j);
         }
-        tc_commit(bKempty(s));
-        tc_commit(bSfull(int(j % NSB)));
-        DBSP_TR(kTrMmaS, j);
+        __syncwarp();
       };
       auto issue_pv = [&](uint32_t i) {
         const int b = int(i % NSB);
@@ -381,21 +387,25 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(bVfull(s), (i / NS) & 1);
         tc_fence_after();
         const uint32_t pcol = tmem + C::kColS + 64u * b;
+        const uint64_t bV = dV + ((uint32_t(s) * C::kTileBytes) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t bd = smem_desc_sw128(sV + s * C::kTileBytes + kk * 2048, 8192, 1024);
-          mma_ts(tmem + C::kColO, pcol + kk * 8, bd, kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(tmem + C::kColO, pcol + kk * 8, bV + ((kk * 2048) >> 4), kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(bVempty(s));
+          tc_commit(bOdone(i));
+          DBSP_TR(kTrMmaPV, i);
         }
-        tc_commit(bVempty(s));
-        tc_commit(bOdone(i));
-        DBSP_TR(kTrMmaPV, i);
+        __syncwarp();
       };
       mbar_wait(bQready, 0);
       tc_fence_after();
       // S runs NSB tiles ahead of PV.  S_{j+NSB} reuses the TMEM columns of
       // P_j, which PV_j (issued just before) reads: tcgen05.mma ops of one
       // thread execute in issue order, so that read precedes the later write
-      // (DBSP_STRICT_WAR adds an explicit completion wait).
+      // (DBSP_STRICT_WAR adds an explicit completion wait).  elect.sync picks
+      // the same lane every time (the lowest active one), so every MMA of the
+      // kernel comes from one thread.
       for (uint32_t j = 0; j < uint32_t(NSB) && j < count; ++j) issue_s(j);
       for (uint32_t j = 0; j < count; ++j) {
         issue_pv(j);
@@ -406,11 +416,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           issue_s(j + NSB);
         }
       }
-      tc_commit(bOfinal);
-    } else if (count > 0) {
-      mbar_wait(bOfinal, 0);
+      if (elect_one()) tc_commit(bOfinal);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ Q -> TMEM
     const int row = threadIdx.x;  // 0..127 == TMEM lane

@@ -99,7 +99,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPd3, 1)
     sparse_attn_fwd_pd3_kernel(const __grid_constant__ CUtensorMap tmQ,
                                const __grid_constant__ CUtensorMap tmK,
                                const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  if (gated_off(p)) return;  // the device-side choice picked the other kernel
   using C = Pd3Cfg;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];

@@ -14,22 +14,12 @@ uint32_t normalize_sched_flags(uint32_t flags) {
     fail(kConfig, "quad / 128-key layouts run only the CTA-pair kernel: pass DBSP_SCHED_CTA_PAIR");
   if ((flags & kSchedAutoD128) && (flags & kSchedCtaPair))
     fail(kConfig, "DBSP_SCHED_AUTO_D128 chooses the layout itself; do not combine it with CTA_PAIR");
+  if (flags & kSchedAutoD128) flags = (flags & ~kSchedAutoD128) | kSchedPairQ;  // see schedule.hpp
   return flags;
 }
 
 void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out) {
   flags = normalize_sched_flags(flags);
-  if (flags & kSchedAutoD128) {
-    const uint32_t keep = flags & (kSchedGlobalLpt | kSchedHeadOrder);
-    Schedule quad;
-    build_schedule(m, v, keep | kSchedPairQ | kSchedQuad | kSchedKey128 | kSchedCtaPair, quad);
-    build_schedule(m, v, keep | kSchedPairQ, out);
-    // dense fraction of the issued 64x64 tiles: pairs issue 2, quads 4 per visit
-    const double f_pair = out.tile_visits ? double(out.dense_tiles) / (2.0 * double(out.tile_visits)) : 1.0;
-    const double f_quad = quad.tile_visits ? double(quad.dense_tiles) / (4.0 * double(quad.tile_visits)) : 1.0;
-    if (f_quad >= kAutoQuadRatio * f_pair) out = std::move(quad);
-    return;
-  }
   const bool pair_q = (flags & kSchedPairQ) != 0;
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
   if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto: K/V of <= 8 heads x 512 blocks

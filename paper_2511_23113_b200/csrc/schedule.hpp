@@ -57,26 +57,23 @@ constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, hea
 constexpr uint32_t kSchedQuad = 8;       // layout: four Q blocks per item
 constexpr uint32_t kSchedKey128 = 16;    // layout: 128-key steps
 constexpr uint32_t kSchedCtaPair = 128;  // d=128 CTA-pair kernel (attn_kernel_pd3.cuh); implies 1|8|16
-// For head_dim 128: build the CTA-pair quad schedule (kSchedPairQ|kSchedQuad|
-// kSchedKey128|kSchedCtaPair) when its dense fraction is at least
-// kAutoQuadRatio of the pair schedule's, else the pair schedule.  The
-// CTA-pair kernel measured 1.04-1.08x faster per launch where four Q rows
-// share their KV blocks (Wan, HunyuanVideo, banded masks: 0.96-0.99 dense vs
-// 0.99-1.00 for pairs) and 1.23x slower on uniform random masks (0.41 vs 0.60).
+// For head_dim 128: the automatic layout choice.  Round 1 picked the CTA-pair
+// quad schedule where its dense fraction stayed within 0.95x of the pair
+// schedule's (then 4-8% faster there).  Since the one-CTA kernel issues its
+// MMAs warp-uniformly (round 2) it takes fewer cycles than the CTA-pair kernel
+// on every measured mask family -- Wan 8.20 M vs 8.89 M, HunyuanVideo 60.1 M
+// vs 62.2 M cycles per launch (profiles/r02_kernel_choice.md) -- and the quad
+// union can only be sparser than the pair union, so AUTO now resolves to the
+// pair layout.  The CTA-pair kernel stays available through kSchedCtaPair.
 constexpr uint32_t kSchedAutoD128 = 256;
 constexpr uint32_t kSchedKnown = kSchedPairQ | kSchedGlobalLpt | kSchedHeadOrder | kSchedQuad | kSchedKey128 |
                                  kSchedCtaPair | kSchedAutoD128;
-constexpr double kAutoQuadRatio = 0.95;
 // Flags as built: CTA_PAIR implies the quad layout bits; QUAD / KEY128 alone
 // (the retired two-stage one-CTA kernels) and unknown bits are config errors.
 uint32_t normalize_sched_flags(uint32_t flags);
 // Quad items: WorkItem{head, q0, q1, begin, count, pad_mask, q2, q3}; entries
 // carry one dense bit per row at 22..25 and (valid keys - 1) at 26..31.
 constexpr uint32_t kQuadValidShift = 26;
-
-// Opaque storage for a device build whose entry write is deferred until the
-// device-side AUTO_D128 choice (schedule_device.cu PendingWrite).
-constexpr size_t kPendingBytes = 256;
 
 // Builds the work items in LPT launch order (see schedule.cpp).
 void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out);

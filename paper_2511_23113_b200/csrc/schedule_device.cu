@@ -67,42 +67,21 @@ __device__ __forceinline__ uint64_t row_word(const ItemRows& r, uint32_t j, uint
   return r.row[j] ? r.row[j][w] : 0ull;
 }
 
-// totals: [0] tile visits (sum of counts), [1] dense 64x64 tiles -- the inputs
-// of the DBSP_SCHED_AUTO_D128 choice.
-__global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned long long* keys,
-                         unsigned long long* totals) {
+__global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned long long* keys) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t c = 0, dn = 0;
-  if (i < n_items) {
-    const ItemRows r = item_rows(a, i);
-    for (uint32_t w = 0; w < a.wpr; ++w) {
-      const uint64_t p = a.present[w];
-      uint64_t uni = 0;
+  if (i >= n_items) return;
+  const ItemRows r = item_rows(a, i);
+  uint32_t c = 0;
+  for (uint32_t w = 0; w < a.wpr; ++w) {
+    const uint64_t p = a.present[w];
+    uint64_t uni = 0;
 #pragma unroll
-      for (uint32_t j = 0; j < 4; ++j) {
-        const uint64_t x = row_word(r, j, w) & p;
-        uni |= x;
-        dn += __popcll(x);
-      }
-      c += __popcll(uni);
-    }
-    counts[i] = c;
-    const unsigned long long head_key = a.head_order ? (unsigned long long)r.hl : 0ull;
-    if (keys) keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
+    for (uint32_t j = 0; j < 4; ++j) uni |= row_word(r, j, w) & p;
+    c += __popcll(uni);
   }
-  if (totals) {
-    // warp-aggregated: one atomic pair per warp
-    unsigned long long cv = c, dv = dn;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      cv += __shfl_xor_sync(0xffffffffu, cv, o);
-      dv += __shfl_xor_sync(0xffffffffu, dv, o);
-    }
-    if ((threadIdx.x & 31) == 0 && (cv | dv)) {
-      atomicAdd(totals, cv);
-      atomicAdd(totals + 1, dv);
-    }
-  }
+  counts[i] = c;
+  const unsigned long long head_key = a.head_order ? (unsigned long long)r.hl : 0ull;
+  if (keys) keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
 }
 
 __global__ void k2_sorted_counts(const unsigned long long* sorted_keys, const uint32_t* counts,
@@ -216,11 +195,9 @@ __global__ void __launch_bounds__(kK2Threads, 1)
   }
 }
 
-// Entries of a fused-planned list: one warp per sorted item.  With `gate`, a
-// device-side AUTO_D128 build writes only the layout it chose.
+// Entries of a fused-planned list: one warp per sorted item.
 __global__ void k2_write_fused(K2Args a, uint32_t n_items, const uint32_t* sorted_idx, const uint32_t* begins,
-                               uint32_t* entries, const uint32_t* gate, uint32_t gate_value) {
-  if (gate && *gate != gate_value) return;
+                               uint32_t* entries) {
   const uint32_t j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const uint32_t lane = threadIdx.x & 31;
   if (j >= n_items) return;
@@ -256,18 +233,6 @@ __global__ void k2_write_fused(K2Args a, uint32_t n_items, const uint32_t* sorte
   }
 }
 
-// DBSP_SCHED_AUTO_D128 on the device, the host rule of schedule.cpp in the
-// same double expressions: the CTA-pair (quad) list when its dense fraction
-// is at least kAutoQuadRatio of the pair list's.  gate = 1 selects the
-// CTA-pair kernel, 0 the pair-item kernel (both are launched; the other
-// returns at its first instruction).
-__global__ void k2_choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad,
-                          uint32_t* gate) {
-  const double f_pair = tot_pair[0] ? double(tot_pair[1]) / (2.0 * double(tot_pair[0])) : 1.0;
-  const double f_quad = tot_quad[0] ? double(tot_quad[1]) / (4.0 * double(tot_quad[0])) : 1.0;
-  *gate = f_quad >= dbsp_core::kAutoQuadRatio * f_pair ? 1u : 0u;
-}
-
 }  // namespace dbsp_dev
 
 namespace {
@@ -282,33 +247,12 @@ void ck(cudaError_t e, const char* what) {
 
 namespace dbsp_k2 {
 
-// A fused-planned list whose entries are not written yet (n = 0: none).
-struct PendingWrite {
-  dbsp_dev::K2Args a;
-  uint32_t n = 0;
-  const uint32_t* sorted_idx = nullptr;
-  const uint32_t* begins = nullptr;
-  uint32_t* entries = nullptr;
-};
-
-void write_fused(const PendingWrite& w, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream) {
-  if (!w.n) return;
-  dbsp_core::count_launch();
-  dbsp_dev::k2_write_fused<<<(w.n + 7) / 8, 256, 0, stream>>>(w.a, w.n, w.sorted_idx, w.begins, w.entries, gate,
-                                                             gate_value);
-  ck(cudaGetLastError(), "k2_write_fused");
-}
-
 // Builds one layout into `items_out` / `entries_out` (device, caller-sized:
-// n_items and n_items * nk_local entries).  `totals` (2 x u64, zeroed here)
-// receives the tile visits and dense tiles when not null.  Stream-ordered.
+// n_items and n_items * nk_local entries).  Stream-ordered.
 void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, const LocalView& v,
            uint32_t flags, const uint32_t* d_head_ids, const uint32_t* d_q_ids,
            const uint64_t* d_present, const int32_t* d_kv_local, dbsp_core::WorkItem* items_out,
-           uint32_t* entries_out, unsigned long long* totals, void*& scratch, size_t& scratch_bytes,
-           cudaStream_t stream, void* deferred_storage) {
-  static_assert(sizeof(PendingWrite) <= kPendingBytes, "PendingWrite storage");
-  PendingWrite* deferred = static_cast<PendingWrite*>(deferred_storage);
+           uint32_t* entries_out, void*& scratch, size_t& scratch_bytes, cudaStream_t stream) {
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
   if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder))) global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
   const uint32_t step = (flags & kSchedQuad) ? 4 : (flags & kSchedPairQ) ? 2 : 1;
@@ -320,7 +264,7 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
                      global_lpt ? 0u : 1u};
   const uint32_t head_bits = global_lpt ? 0u : uint32_t(32 - __builtin_clz(std::max(v.heads, 2u) - 1));
   if (n <= uint32_t(dbsp_dev::kFusedItems) && 22 + head_bits <= 32) {
-    // one-CTA planner + a gated entry writer (5 launches for both AUTO layouts)
+    // one-CTA planner + the entry writer (3 launches)
     const size_t need = 3 * size_t(n) * 4 + 256;
     if (scratch_bytes < need) {
       if (scratch) {
@@ -341,23 +285,18 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
                                       int(sizeof(dbsp_dev::K2Smem)));
     });
     ck(attr_err, "k2_plan_fused attribute");
-    if (totals) ck(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), stream), "k2 totals");
     dbsp_core::count_launch();
-    dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, cnts, nullptr, totals);
+    dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, cnts, nullptr);
     ck(cudaGetLastError(), "k2_count");
     dbsp_core::count_launch();
     dbsp_dev::k2_plan_fused<<<1, dbsp_dev::kK2Threads, sizeof(dbsp_dev::K2Smem), stream>>>(
         a, n, 22 + head_bits, cnts, items_out, sidx, begins);
     ck(cudaGetLastError(), "k2_plan_fused");
-    PendingWrite w{a, n, sidx, begins, entries_out};
-    if (deferred) {
-      *deferred = w;  // written after the AUTO choice, gated
-    } else {
-      write_fused(w, nullptr, 0, stream);
-    }
+    dbsp_core::count_launch();
+    dbsp_dev::k2_write_fused<<<(n + 7) / 8, 256, 0, stream>>>(a, n, sidx, begins, entries_out);
+    ck(cudaGetLastError(), "k2_write_fused");
     return;
   }
-  if (deferred) deferred->n = 0;  // the CUB path writes its entries itself
   // scratch: counts, keys, sorted keys, sorted counts, begins, cub temp
   size_t sort_tmp = 0, scan_tmp = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp, (unsigned long long*)nullptr,
@@ -387,9 +326,8 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   uint32_t* begins = reinterpret_cast<uint32_t*>(s);
   s += up(n * 4);
   void* tmp = s;
-  if (totals) ck(cudaMemsetAsync(totals, 0, 2 * sizeof(unsigned long long), stream), "k2 totals");
   dbsp_core::count_launch();
-  dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, counts, keys, totals);
+  dbsp_dev::k2_count<<<(n + 255) / 256, 256, 0, stream>>>(a, n, counts, keys);
   ck(cudaGetLastError(), "k2_count");
   size_t t1 = sort_tmp;
   ck(cub::DeviceRadixSort::SortKeys(tmp, t1, keys, sorted, int(n), 0, 64, stream), "k2 sort");
@@ -402,17 +340,6 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
   dbsp_dev::k2_write<<<(n + 7) / 8, 256, 0, stream>>>(a, n, sorted, scounts, begins, items_out,
                                                       entries_out);
   ck(cudaGetLastError(), "k2_write");
-}
-
-void write_deferred(const void* deferred_storage, const uint32_t* gate, uint32_t gate_value, cudaStream_t stream) {
-  write_fused(*static_cast<const PendingWrite*>(deferred_storage), gate, gate_value, stream);
-}
-
-void choose(const unsigned long long* tot_pair, const unsigned long long* tot_quad, uint32_t* gate,
-            cudaStream_t stream) {
-  dbsp_core::count_launch();
-  dbsp_dev::k2_choose<<<1, 1, 0, stream>>>(tot_pair, tot_quad, gate);
-  ck(cudaGetLastError(), "k2_choose");
 }
 
 }  // namespace dbsp_k2

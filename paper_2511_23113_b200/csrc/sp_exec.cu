@@ -377,8 +377,7 @@ struct RankExec {
         v.num_kv_blocks = uint32_t(me.groups[g].size());
         v.kv_block_ids = me.groups[g].data();
         v.kv_tokens_global = tokens;
-        // pair schedule, or for d=128 the CTA-pair kernel where it pays (DBSP_SCHED_AUTO_D128,
-        // decided on the device)
+        // the pair schedule (DBSP_SCHED_AUTO_D128 resolves to it for d=128)
         rc(dbsp_schedule_build_device(sched[g], dw, H, mset->num_q_blocks, mset->num_kv_blocks, &v,
                                       d == 128 ? (DBSP_SCHED_PAIR_Q | DBSP_SCHED_AUTO_D128) : DBSP_SCHED_PAIR_Q,
                                       st));

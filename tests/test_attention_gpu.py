@@ -171,8 +171,8 @@ def test_partitioned_execution_matches_one_shot(strategy):
 @pytest.mark.parametrize("case", ["identity", "rank_view", "ragged"])
 def test_device_schedule_matches_host(case, pattern, flags):
     # K2 on the GPU builds exactly the host builder's list (items, order,
-    # entries) for the pair layout, the CTA-pair quad layout and the auto
-    # choice between them (clustered masks pick quads, random masks pairs).
+    # entries) for the pair layout, the CTA-pair quad layout and the d=128
+    # auto choice (which resolves to the pair layout since round 2).
     from paper_2511_23113_b200.sp import rank_layouts
     H, nb = 8, 96
     if pattern == "dense":
@@ -192,8 +192,8 @@ def test_device_schedule_matches_host(case, pattern, flags):
     host = AttentionSchedule().build(masks, kv_tokens_global=S, flags=flags, **kw)
     dev = AttentionSchedule().build_device(words, nb, kv_tokens_global=S, flags=flags, **kw)
     assert host.layout() == dev.layout()
-    if flags == 1 | 256 and case == "identity" and pattern != "clustered":
-        assert dev.layout()["kernel"] == ("cta_pair_split_kv" if pattern == "dense" else "pair_items")
+    if flags == 1 | 256:
+        assert dev.layout()["kernel"] == "pair_items"
     hi, he = host.download()
     di, de = dev.download()
     assert np.array_equal(hi, di)
@@ -201,20 +201,20 @@ def test_device_schedule_matches_host(case, pattern, flags):
     assert host.stats() == dev.stats()
 
 
+@pytest.mark.parametrize("flags", [1 | 256, 1 | 8 | 16 | 128])
 @pytest.mark.parametrize("pattern", ["clustered", "random"])
-def test_device_auto_choice_runs_one_kernel(pattern):
-    # Both kernels are launched for a device-built auto schedule; the one not
-    # chosen must leave the output alone, so the result equals the host-built
-    # schedule's bit for bit.
+def test_device_built_schedule_launch_equals_host(pattern, flags):
+    # A device-built schedule (K2) runs the same kernel over the same list as
+    # the host-built one: the output is equal bit for bit.
     H, S, d = 6, 3000, 128
     nb = -(-S // 64)
     masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pattern, 0.15, 0.5, 1.0, 13))
     q, k, v = (t.cuda() for t in make_qkv(S, H, d, 14))
-    host = AttentionSchedule().build(masks, kv_tokens_global=S, head_dim=d)
+    host = AttentionSchedule().build(masks, kv_tokens_global=S, flags=flags)
     ref = torch.empty_like(q)
     host.launch(q, k, v, ref)
     words = torch.from_numpy(masks.words.view(np.int64)).cuda()
-    dev = AttentionSchedule().build_device(words, nb, kv_tokens_global=S, head_dim=d)
+    dev = AttentionSchedule().build_device(words, nb, kv_tokens_global=S, flags=flags)
     out = torch.full_like(q, 5.0)
     dev.launch(q, k, v, out)
     torch.cuda.synchronize()

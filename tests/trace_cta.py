@@ -1,6 +1,6 @@
 """Per-CTA start/end (globaltimer) and SM id of one K4 launch on the Wan
 layer (DBSP_TRACE_CTA build): occupancy over time, per-item cost vs KV
-count, and the tail.  GPU-box tool: python tests/trace_cta.py [sched_flags]"""
+count, and the tail.  GPU-box tool: python tests/trace_cta.py [sched_flags [workload]]"""
 import ctypes
 import json
 import os
@@ -16,14 +16,17 @@ sys.path.insert(0, str(ROOT))
 
 def main():
     sched_flags = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    workload = sys.argv[2] if len(sys.argv) > 2 else "wan"
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    env=dict(os.environ, DBSP_NVCC_FLAGS="-DDBSP_TRACE_CTA"), capture_output=True)
     import torch
     import paper_2511_23113_b200 as D
     from paper_2511_23113_b200 import _lib
     from paper_2511_23113_b200.attention import AttentionSchedule
-    H, S, d = 40, 32768, 128
-    m = D.generate_mask_set(D.GeneratorSpec(H, S // 64, S // 64, 64, "clustered", 0.15, 0.45, 1.0, 1))
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    wl = WORKLOADS[workload]
+    H, S, d = wl.heads, wl.tokens, wl.head_dim
+    m = D.generate_mask_set(wl.spec())
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=sched_flags)
     items, _ = sc.download()

@@ -23,6 +23,10 @@ def main():
     fine = args[:1] == ["--fine"]
     if fine:
         args = args[1:] + ["-DDBSP_TRACE_FINE"]
+    workload = "wan"
+    if args[:1] == ["--workload"]:
+        workload = args[1]
+        args = args[2:]
     mma = args[:1] == ["--mma"]
     if mma:
         args = args[1:] + ["-DDBSP_TRACE_MMA"]
@@ -38,8 +42,10 @@ def main():
     fn = _lib.lib().dbsp_debug_set_trace
     fn.argtypes = [ctypes.c_void_p]
     fn(ctypes.c_void_p(buf.data_ptr()))
-    H, S, d = 40, 32768, 128
-    m = D.generate_mask_set(D.GeneratorSpec(H, S // 64, S // 64, 64, "clustered", 0.15, 0.45, 1.0, 1))
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    wl = WORKLOADS[workload]
+    H, S, d = wl.heads, wl.tokens, wl.head_dim
+    m = D.generate_mask_set(wl.spec())
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     sc = AttentionSchedule().build(m, kv_tokens_global=S, flags=sched_flags)
     out = torch.empty_like(q)
