@@ -5,7 +5,8 @@ reach on this box, power cap included", the context for K4's roofline
 fraction.  Libraries: torch SDPA with the cuDNN backend (cuDNN's Blackwell
 FMHA) and with the flash backend (FlashAttention-2, mma.sync).  FLOPs =
 4 * S_q * S_k * d * H (QK^T + PV), as for K4's dense tiles.
-GPU-box tool: python tests/dense_lib_compare.py > out.json"""
+GPU-box tool: python tests/dense_lib_compare.py [workload] > out.json (default wan; the
+sparse line uses the workload's own benchmark masks)."""
 import json
 import sys
 from pathlib import Path
@@ -37,10 +38,12 @@ def timed(fn, reps=10, warm=3):
 
 
 def main():
-    S, H, d = 32768, 40, 128
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "wan"]
+    S, H, d = wl.tokens, wl.heads, wl.head_dim
     g = torch.Generator(device="cuda").manual_seed(1234)
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
-    out = {"shape": {"tokens": S, "heads": H, "head_dim": d}}
+    out = {"workload": wl.name, "shape": {"tokens": S, "heads": H, "head_dim": d}}
     dense_flop = 4.0 * S * S * d * H
     # libraries want [B, H, S, d]; the transposed views are what they read
     qt, kt, vt = (t.permute(1, 0, 2).unsqueeze(0) for t in (q, k, v))
@@ -53,9 +56,9 @@ def main():
         except Exception as e:  # backend not available for this layout / build
             r = {"error": str(e).splitlines()[0][:200]}
         out[f"sdpa_{name}_dense"] = r
-    nb = S // 64
+    nb = -(-S // 64)
     for label, spec in (("k4_dense", D.GeneratorSpec(H, nb, nb, 64, "random", 1.0, 1.0, 1.0, 1)),
-                        ("k4_clustered_0.30", D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 1))):
+                        ("k4_benchmark_masks", wl.spec())):
         masks = D.generate_mask_set(spec)
         flop = 4.0 * 64 * 64 * d * D.total_blocks(masks)
         sc = AttentionSchedule().build(masks, kv_tokens_global=S)

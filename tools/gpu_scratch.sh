@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/s_gputests.log 2>&1; echo "gpu tests rc=$?"; tail -3 gpurun_out/s_gputests.log
-timeout 900 python bench.py > gpurun_out/s_bench.json 2> gpurun_out/s_bench.err; echo "bench rc=$?"
-timeout 900 python bench.py --workload cogvideox --sp-sim 0 > gpurun_out/s_bench_cog.json 2> gpurun_out/s_bench_cog.err; echo "bench cog rc=$?"
+for wl in wan cogvideox hunyuan; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sparse_attn_fwd -s 3 -c 1 -o gpurun_out/r02b_${wl}_full python bench.py --workload $wl --steps 1 --warmup 3 --no-cpu-baseline --sp-sim 0 > gpurun_out/r02b_ncu_$wl.log 2>&1; echo "$wl ncu rc=$?"
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02b_launches_wan.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --sp-sim 0 > /dev/null 2>&1; echo "launches rc=$?"
