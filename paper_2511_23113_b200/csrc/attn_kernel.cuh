@@ -97,106 +97,47 @@ constexpr int kTraceBlocks = 16, kTraceTiles = 256;
   do {                 \
   } while (0)
 #endif
+// DBSP_TRACE_FINE1 (tests/trace_kernel.py --fine1 [--warp W]): softmax warp W
+// stamps the phases of its step into slots 4-7 -- S loaded, max known, exps
+// done, P stored -- instead of the hi-half and load events.
+#if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
+#ifndef DBSP_TRACE_WARP
+#define DBSP_TRACE_WARP 0
+#endif
+#define DBSP_TRF(ev, j)                                        \
+  do {                                                         \
+    if (warp == DBSP_TRACE_WARP && lane == 0) DBSP_TR(ev, j); \
+  } while (0)
+#define DBSP_TRC(ev, j)         \
+  do {                          \
+    if ((ev) < 4) DBSP_TR(ev, j); \
+  } while (0)
+#else
+#define DBSP_TRF(ev, j) \
+  do {                  \
+  } while (0)
+#define DBSP_TRC(ev, j) DBSP_TR(ev, j)
+#endif
 
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain
 // exp2 pairs (of every 8) computed on the FMA pipe (exp2_poly3_pair) instead
-// of MUFU.  Measured (tests/kernel_sweep.py): d=64 is MUFU-bound and runs
-// 1.83 ms with 2 of 8 vs 1.94 ms with none on the CogVideoX layer; d=128 is
-// smem-port bound and only slows down (6.47 vs 6.22 ms on Wan).
+// of MUFU.  Measured: d=64 is MUFU-bound -- on the CogVideoX layer 1.94 ms
+// with none (round 1, tests/kernel_sweep.py), and per launch (ncu cycles,
+// tests/variant_cycles.py, round 2) 3.07 M cycles with 2 of 8 vs 2.99 M with
+// 3 of 8 (4 of 8 is slower again, profiles/r02_d64_poly_sweep.log); d=128 is
+// smem-port and power bound and only slows down (Wan: 5.71 / 5.97 / 6.32 ms
+// for 0 / 1 / 2 of 8).
 template <int D>
 __host__ __device__ constexpr int poly_pairs() {
 #ifdef DBSP_POLY_N
   return DBSP_POLY_N;
 #else
-  return D == 64 ? 2 : 0;
+  return D == 64 ? 3 : 0;
 #endif
 }
 
-
-// Row epilogue shared by the two-stage kernels: O (TMEM columns at `ocol`, this
-// thread's lane) / l -> bf16 out and LSE, or the ring-accumulator merge (K5)
-// when p.mode has kModeAccumulate.  `have_o` false: the row saw no KV tile.
-template <int D>
-__device__ __forceinline__ void finish_row(const AttnParams& p, uint32_t ocol, bool have_o, bool live,
-                                           float m, float l, uint32_t token, uint32_t head) {
-  const float inv_l = l > 0.f ? 1.f / l : 0.f;
-  const float kLn2 = 0.6931471805599453f;
-  const float lse_new = l > 0.f ? (m + log2f(l)) * kLn2 : -INFINITY;
-  const size_t orow = (size_t(token) * p.heads + head) * D;
-  const size_t lidx = size_t(head) * p.q_tokens + token;
-  bool live_out = live;
-  __nv_bfloat16* const orow_ptr = out_row_ptr<D>(p, token, head, live_out);
-
-  float c_old = 0.f, c_new = inv_l, lse_out = lse_new;
-  const bool acc = (p.mode & kModeAccumulate) != 0;
-  if (acc) {
-    const float lse_old = live ? p.lse_acc[lidx] : -INFINITY;
-    const float mx = fmaxf(lse_old, lse_new);
-    if (mx == -INFINITY) {
-      c_old = 0.f;
-      c_new = 0.f;
-      lse_out = -INFINITY;
-    } else {
-      const float w_old = __expf(lse_old - mx);
-      const float w_new = __expf(lse_new - mx);
-      const float den = w_old + w_new;
-      c_old = w_old / den;
-      c_new = w_new * inv_l / den;
-      lse_out = mx + __logf(den);
-    }
-  }
-  const bool write_bf16 = !acc || (p.mode & kModeFinalize);
-#pragma unroll
-  for (int c = 0; c < D / 32; ++c) {
-    uint32_t o[32];
-    if (have_o) {
-      tmem_ld32(ocol + c * 32, o);
-      tmem_ld_wait();
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = 0u;
-    }
-    if (!live) continue;
-    float r[32];
-    if (acc) {
-      float4* pa = reinterpret_cast<float4*>(p.o_acc + orow + c * 32);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float4 a = pa[i];
-        a.x = a.x * c_old + __uint_as_float(o[4 * i + 0]) * c_new;
-        a.y = a.y * c_old + __uint_as_float(o[4 * i + 1]) * c_new;
-        a.z = a.z * c_old + __uint_as_float(o[4 * i + 2]) * c_new;
-        a.w = a.w * c_old + __uint_as_float(o[4 * i + 3]) * c_new;
-        pa[i] = a;
-        r[4 * i + 0] = a.x;
-        r[4 * i + 1] = a.y;
-        r[4 * i + 2] = a.z;
-        r[4 * i + 3] = a.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) r[i] = __uint_as_float(o[i]) * inv_l;
-    }
-    if (write_bf16 && live_out) {
-      uint4* po = reinterpret_cast<uint4*>(orow_ptr + c * 32);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        po[i] = make_uint4(pack_bf16x2(r[8 * i + 0], r[8 * i + 1]),
-                           pack_bf16x2(r[8 * i + 2], r[8 * i + 3]),
-                           pack_bf16x2(r[8 * i + 4], r[8 * i + 5]),
-                           pack_bf16x2(r[8 * i + 6], r[8 * i + 7]));
-    }
-  }
-  if (live) {
-    if (acc)
-      p.lse_acc[lidx] = lse_out;
-    else if (p.lse)
-      p.lse[lidx] = lse_new;
-  }
-  if (p.out_peers) __threadfence_system();  // peer stores complete before the kernel ends
-}
 
 template <int D>
 struct KCfg {
@@ -229,7 +170,7 @@ struct KCfg {
   static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
 };
 
-template <int D>
+template <int D, int POLY = poly_pairs<D>()>
 __global__ void __launch_bounds__(kThreads, 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmK,
@@ -332,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = int(j % NS);
         mbar_wait(bKempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmK, sK + s * C::kTileBytes, bKfull(s), j);
-        if (lane == 0) DBSP_TR(kTrLoadK, j);
+        if (lane == 0) DBSP_TRC(kTrLoadK, j);
       };
       load_k(0);
       for (uint32_t j = 0; j < count; ++j) {
@@ -340,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int s = int(j % NS);
         mbar_wait(bVempty(s), ((j / NS) & 1) ^ 1);
         load_tile(&tmV, sV + s * C::kTileBytes, bVfull(s), j);
-        if (lane == 0) DBSP_TR(kTrLoadV, j);
+        if (lane == 0) DBSP_TRC(kTrLoadV, j);
       }
     }
     __syncwarp();
@@ -468,13 +409,17 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t scol = tmem + lane_off + C::kColS + 64u * b;
       mbar_wait(bSfull(b), (j / NSB) & 1);
       tc_fence_after();
+#if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
+      DBSP_TRF(kTrSoftStart, j);
+#else
       if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftStart : kTrSoftStartHi, j);
-      uint32_t pk[32];
+#endif
       if (dense) {
         uint32_t sa[32], sb[32];
         tmem_ld32(scol, sa);
         tmem_ld32(scol + 32, sb);
         tmem_ld_wait();
+        DBSP_TRF(4, j);
         const uint32_t valid = ((e >> dbsp_core::kEntryValidShift) & 63u) + 1u;
         float v[64];
 #pragma unroll
@@ -487,70 +432,91 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int i = 0; i < 64; ++i)
             if (uint32_t(i) >= valid) v[i] = -INFINITY;
         }
-        // Row max as a 3-input-max tree (FMNMX3): depth 5, not a 64-long chain.
-        float mx[8];
+        // Row max (log2 domain) as a 3-input-max tree (FMNMX3): depth 5, not a
+        // 64-long chain.
+        auto row_max2 = [&]() {
+          float mx[8];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          mx[a] = fmax3f(v[8 * a], v[8 * a + 1], v[8 * a + 2]);
-          mx[a] = fmax3f(mx[a], v[8 * a + 3], v[8 * a + 4]);
-          mx[a] = fmax3f(mx[a], v[8 * a + 5], v[8 * a + 6]);
-          mx[a] = fmaxf(mx[a], v[8 * a + 7]);
-        }
-        const float mt = fmaxf(fmax3f(mx[0], mx[1], mx[2]),
-                               fmax3f(fmax3f(mx[3], mx[4], mx[5]), mx[6], mx[7]));
-        const float mt2 = mt * sl2;
-        const bool resc = mt2 > m + kRescaleThreshold;
-        const bool need_o = resc && (m != -INFINITY);
-        float alpha = 1.f;
-        if (resc) {
-          alpha = fast_exp2(m - mt2);
-          l *= alpha;
-          m = mt2;
-        }
-        if (__any_sync(0xffffffffu, need_o)) {
-          // O must be quiescent.  With one S buffer, S_j was issued after
-          // PV_{j-1}, so its completion (seen above) implies PV_{j-1}'s.
-          if (NSB > 1 && j > 0) {
-            mbar_wait(bOdone(j - 1), ((j - 1) >> 1) & 1);
-            tc_fence_after();
+          for (int a = 0; a < 8; ++a) {
+            mx[a] = fmax3f(v[8 * a], v[8 * a + 1], v[8 * a + 2]);
+            mx[a] = fmax3f(mx[a], v[8 * a + 3], v[8 * a + 4]);
+            mx[a] = fmax3f(mx[a], v[8 * a + 5], v[8 * a + 6]);
+            mx[a] = fmaxf(mx[a], v[8 * a + 7]);
           }
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_off + C::kColO + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(tmem + lane_off + C::kColO + c * 32, o);
+          return fmaxf(fmax3f(mx[0], mx[1], mx[2]), fmax3f(fmax3f(mx[3], mx[4], mx[5]), mx[6], mx[7])) * sl2;
+        };
+        // Raise the running max to mt2 when it grows by more than the
+        // threshold; O and l are rescaled by the same factor.
+        auto raise_max = [&](float mt2) {
+          const bool resc = mt2 > m + kRescaleThreshold;
+          const bool need_o = resc && (m != -INFINITY);
+          float alpha = 1.f;
+          if (resc) {
+            alpha = fast_exp2(m - mt2);
+            l *= alpha;
+            m = mt2;
           }
-        }
-        // Packed f32x2 FMA/add (FFMA2/FADD2): half the non-MUFU issue slots.
-        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          if (__any_sync(0xffffffffu, need_o)) {
+            // O must be quiescent.  With one S buffer, S_j was issued after
+            // PV_{j-1}, so its completion (seen above) implies PV_{j-1}'s.
+            if (NSB > 1 && j > 0) {
+              mbar_wait(bOdone(j - 1), ((j - 1) >> 1) & 1);
+              tc_fence_after();
+            }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
-          float2 pp;
-          if ((i & 7) < poly_pairs<D>()) {  // FA4-style MUFU offload
-            pp = exp2_poly3_pair(x);
-          } else {
-            pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t o[32];
+              tmem_ld32(tmem + lane_off + C::kColO + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tmem + lane_off + C::kColO + c * 32, o);
+            }
           }
-          acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
-          pk[i] = pack_bf16x2(pp.x, pp.y);
-        }
-        const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
-        l += a2.x + a2.y;
-      } else {
+        };
+        // P = 2^(S*scale - m) as packed bf16; returns the row sum.  Packed
+        // f32x2 FMA/add (FFMA2/FADD2): half the non-MUFU issue slots.
+        uint32_t pk[32];
+        auto exps = [&]() {
+          const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+          float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = 0u;
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
+            float2 pp;
+            if ((i & 7) < POLY) {  // FA4-style MUFU offload
+              pp = exp2_poly3_pair(x);
+            } else {
+              pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            }
+            acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
+            pk[i] = pack_bf16x2(pp.x, pp.y);
+          }
+          const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
+          return a2.x + a2.y;
+        };
+        const float mt2 = row_max2();
+        DBSP_TRF(5, j);
+        raise_max(mt2);
+        l += exps();
+        DBSP_TRF(6, j);
+        tmem_st32(scol, pk);
+      } else {  // this half's rows have no keys in the block: P = 0
+        uint32_t z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0u;
+        tmem_st32(scol, z);
       }
-      tmem_st32(scol, pk);
       tmem_st_wait();
+      DBSP_TRF(7, j);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bPfull(b));
+#if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
+      DBSP_TRF(kTrSoftEnd, j);
+#else
       if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftEnd : kTrSoftEndHi, j);
+#endif
     }
 
     // ------------------------------------------------------------ epilogue

@@ -99,6 +99,9 @@ int main() {
     run<256, false, 4>("SS M128 N256 K16 x4", c);
     run<128, true, 64>("TS M128 N128 K16 x64", c);
     run<64, false, 64>("SS M128 N64 K16 x64", c);
+    run<64, true, 64>("TS M128 N64 K16 x64", c);
+    run<64, true, 4>("TS M128 N64 K16 x4", c);
+    run<64, true, 1>("TS M128 N64 K16 x1", c);
   }
   return 0;
 }

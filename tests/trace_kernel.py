@@ -27,6 +27,14 @@ def main():
     if args[:1] == ["--workload"]:
         workload = args[1]
         args = args[2:]
+    fine1 = args[:1] == ["--fine1"]
+    if fine1:
+        args = args[1:] + ["-DDBSP_TRACE_FINE1"]
+        if args[:1] == ["--warp"]:
+            args = args[2:] + [f"-DDBSP_TRACE_WARP={args[1]}"]
+    fine2 = args[:1] == ["--fine2"]
+    if fine2:
+        args = args[1:] + ["-DDBSP_TRACE_FINE2"]
     mma = args[:1] == ["--mma"]
     if mma:
         args = args[1:] + ["-DDBSP_TRACE_MMA"]
@@ -63,6 +71,47 @@ def main():
             print(f"block {b}: steps={n}")
             for j in range(min(n, 14)):
                 print("  t=%2d " % j + " ".join(f"{nm}={int(t[j, e] - base):7d}" for e, nm in enumerate(names)))
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
+    if fine2:
+        stats = {}
+        for b in range(B):
+            t = tr[b].astype(np.int64)
+            n = int((t[:, 0] > 0).sum())
+            if n < 8:
+                continue
+            t = t[2:n]
+            ends = t[:, 4:8]
+            ok = (ends > 0).all(axis=1)
+            ends = ends[ok]
+            first = ends.min(axis=1)
+            for w in range(4):
+                stats.setdefault(f"warp{w}_after_first", []).append(float(np.median(ends[:, w] - first)))
+            stats.setdefault("last_minus_first", []).append(float(np.median(ends.max(axis=1) - first)))
+            stats.setdefault("last_is_warp", []).append(float(np.bincount(ends.argmax(axis=1), minlength=4).argmax()))
+        print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
+    if fine1:
+        stats = {}
+        for b in range(B):
+            t = tr[b].astype(np.int64)
+            n = int((t[:, 0] > 0).sum())
+            if n < 8:
+                continue
+            t = t[2:n]
+            dense = t[:, 4] > 0  # steps where this warp's rows were dense
+            t = t[dense]
+            for key, arr in [("ld_S", t[:, 4] - t[:, 0]), ("max", t[:, 5] - t[:, 4]),
+                             ("exps", t[:, 6] - t[:, 5]), ("store_wait", t[:, 7] - t[:, 6]),
+                             ("fence_arrive", t[:, 1] - t[:, 7]), ("softmax", t[:, 1] - t[:, 0]),
+                             ("wait_next_S", t[1:, 0] - t[:-1, 1]), ("period", np.diff(t[:, 0])),
+                             ("P_to_PV_issued", t[:, 3] - t[:, 1]),
+                             ("S_issued_to_soft_start", t[:, 0] - t[:, 2])]:
+                stats.setdefault(key, []).append(float(np.median(arr)))
+        print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
         subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                        capture_output=True)
         return
