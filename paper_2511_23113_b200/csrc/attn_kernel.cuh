@@ -85,7 +85,15 @@ __device__ __forceinline__ void clock_probe_mark(const AttnParams& p, int slot) 
 // Event slots of the optional per-tile trace (DBSP_TRACE).
 enum : int { kTrSoftStart = 0, kTrSoftEnd, kTrMmaS, kTrMmaPV, kTrSoftStartHi, kTrSoftEndHi,
              kTrLoadK, kTrLoadV, kTrEvents };
+#ifdef DBSP_TRACE_EXPS
+// Exp-phase overlap of co-resident CTAs (tests/trace_kernel.py --exps): every
+// CTA of the first wave; per step, each softmax warp w stamps the start and end
+// of its exp loop into slots 2w, 2w+1; tile slot kTraceTiles-1 holds the
+// warps' %warpid (slots 0-3) and %smid (slot 4).
+constexpr int kTraceBlocks = 296, kTraceTiles = 128;
+#else
 constexpr int kTraceBlocks = 16, kTraceTiles = 256;
+#endif
 #ifdef DBSP_TRACE
 #define DBSP_TR(ev, j)                                                                         \
   do {                                                                                         \
@@ -100,7 +108,14 @@ constexpr int kTraceBlocks = 16, kTraceTiles = 256;
 // DBSP_TRACE_FINE1 (tests/trace_kernel.py --fine1 [--warp W]): softmax warp W
 // stamps the phases of its step into slots 4-7 -- S loaded, max known, exps
 // done, P stored -- instead of the hi-half and load events.
-#if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
+#if defined(DBSP_TRACE) && defined(DBSP_TRACE_EXPS)
+#define DBSP_TRF(ev, j) \
+  do {                  \
+  } while (0)
+#define DBSP_TRC(ev, j) \
+  do {                  \
+  } while (0)
+#elif defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
 #ifndef DBSP_TRACE_WARP
 #define DBSP_TRACE_WARP 0
 #endif
@@ -317,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           }
           tc_commit(bKempty(s));
           tc_commit(bSfull(int(j % NSB)));
-          DBSP_TR(kTrMmaS, j);
+          DBSP_TRC(kTrMmaS, j);
         }
         __syncwarp();
       };
@@ -335,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mma_ts(tmem + C::kColO, pcol + kk * 8, bV + ((kk * 2048) >> 4), kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
           tc_commit(bVempty(s));
           tc_commit(bOdone(i));
-          DBSP_TR(kTrMmaPV, i);
+          DBSP_TRC(kTrMmaPV, i);
         }
         __syncwarp();
       };
@@ -389,6 +404,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (lane == 0) mbar_arrive(bQready);
     }
 
+#ifdef DBSP_TRACE_EXPS
+    if (lane == 0 && p.trace && blockIdx.x < kTraceBlocks) {
+      unsigned long long* hdr = p.trace + (size_t(blockIdx.x) * kTraceTiles + kTraceTiles - 1) * kTrEvents;
+      uint32_t wid;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      hdr[warp] = wid;
+      if (warp == 0) hdr[4] = smid();
+    }
+#endif
     // ------------------------------------------------------------ softmax
     const uint32_t dense_bit = upper ? dbsp_core::kEntryDenseB : dbsp_core::kEntryDenseA;
     const float sl2 = p.scale_log2;
@@ -412,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
       DBSP_TRF(kTrSoftStart, j);
 #else
-      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftStart : kTrSoftStartHi, j);
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TRC(warp == 0 ? kTrSoftStart : kTrSoftStartHi, j);
 #endif
       if (dense) {
         uint32_t sa[32], sb[32];
@@ -498,7 +522,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         const float mt2 = row_max2();
         DBSP_TRF(5, j);
         raise_max(mt2);
+#ifdef DBSP_TRACE_EXPS
+        if (lane == 0 && j + 1 < uint32_t(kTraceTiles)) DBSP_TR(2 * warp, j);
+#endif
         l += exps();
+#ifdef DBSP_TRACE_EXPS
+        if (lane == 0 && j + 1 < uint32_t(kTraceTiles)) DBSP_TR(2 * warp + 1, j);
+#endif
         DBSP_TRF(6, j);
         tmem_st32(scol, pk);
       } else {  // this half's rows have no keys in the block: P = 0
@@ -515,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #if defined(DBSP_TRACE) && defined(DBSP_TRACE_FINE1)
       DBSP_TRF(kTrSoftEnd, j);
 #else
-      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TR(warp == 0 ? kTrSoftEnd : kTrSoftEndHi, j);
+      if (lane == 0 && (warp == 0 || warp == 2)) DBSP_TRC(warp == 0 ? kTrSoftEnd : kTrSoftEndHi, j);
 #endif
     }
 

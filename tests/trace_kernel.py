@@ -35,6 +35,9 @@ def main():
     fine2 = args[:1] == ["--fine2"]
     if fine2:
         args = args[1:] + ["-DDBSP_TRACE_FINE2"]
+    exps_mode = args[:1] == ["--exps"]
+    if exps_mode:
+        args = args[1:] + ["-DDBSP_TRACE_EXPS"]
     mma = args[:1] == ["--mma"]
     if mma:
         args = args[1:] + ["-DDBSP_TRACE_MMA"]
@@ -45,7 +48,7 @@ def main():
     import paper_2511_23113_b200 as D
     from paper_2511_23113_b200 import _lib
     from paper_2511_23113_b200.attention import AttentionSchedule
-    B, T, E = 16, 256, 8
+    B, T, E = (296, 128, 8) if exps_mode else (16, 256, 8)
     buf = torch.zeros(B * T * E, dtype=torch.int64, device="cuda")
     fn = _lib.lib().dbsp_debug_set_trace
     fn.argtypes = [ctypes.c_void_p]
@@ -91,6 +94,11 @@ def main():
             stats.setdefault("last_minus_first", []).append(float(np.median(ends.max(axis=1) - first)))
             stats.setdefault("last_is_warp", []).append(float(np.bincount(ends.argmax(axis=1), minlength=4).argmax()))
         print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
+        subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
+                       capture_output=True)
+        return
+    if exps_mode:
+        exps_overlap_report(tr)
         subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                        capture_output=True)
         return
@@ -150,6 +158,46 @@ def main():
     print(json.dumps({k: float(np.median(v)) for k, v in stats.items()}))
     subprocess.run([sys.executable, str(ROOT / "paper_2511_23113_b200" / "build.py"), "-f"], check=True,
                    capture_output=True)
+
+
+def exps_overlap_report(tr):
+    """DBSP_TRACE_EXPS: how much of one CTA's exp loop overlaps the exp loop of
+    the other CTA's softmax warp on the same SM sub-partition (1 = lockstep,
+    0 = perfectly staggered), and the exp-loop length when overlapped vs alone."""
+    B, T, _ = tr.shape
+    hdr = tr[:, T - 1, :]
+    by_sm = {}
+    for b in range(B):
+        if hdr[b, 4] == 0 and b > 0:
+            continue
+        by_sm.setdefault(int(hdr[b, 4]), []).append(b)
+    fr, len_ov, len_alone = [], [], []
+    for sm, blocks in by_sm.items():
+        if len(blocks) != 2:
+            continue
+        a, c = blocks
+        for wa in range(4):
+            smsp = int(hdr[a, wa]) % 4
+            wc = [w for w in range(4) if int(hdr[c, w]) % 4 == smsp]
+            if not wc:
+                continue
+            ia = [(int(tr[a, j, 2 * wa]), int(tr[a, j, 2 * wa + 1])) for j in range(T - 1) if tr[a, j, 2 * wa] > 0]
+            ic = [(int(tr[c, j, 2 * wc[0]]), int(tr[c, j, 2 * wc[0] + 1])) for j in range(T - 1)
+                  if tr[c, j, 2 * wc[0]] > 0]
+            if len(ia) < 8 or len(ic) < 8:
+                continue
+            t0, t1 = max(ia[0][0], ic[0][0]), min(ia[-1][1], ic[-1][1])
+            for s0, s1 in ia:
+                if s0 < t0 or s1 > t1 or s1 <= s0:
+                    continue
+                ov = sum(max(0, min(s1, e1) - max(s0, e0)) for e0, e1 in ic)
+                fr.append(ov / (s1 - s0))
+                (len_ov if ov / (s1 - s0) > 0.5 else len_alone).append(s1 - s0)
+    print(json.dumps({"pairs_measured": len(fr), "overlap_frac_median": float(np.median(fr)) if fr else None,
+                      "overlap_frac_mean": float(np.mean(fr)) if fr else None,
+                      "frac_mostly_overlapped": float(np.mean(np.array(fr) > 0.5)) if fr else None,
+                      "exps_cycles_when_overlapped": float(np.median(len_ov)) if len_ov else None,
+                      "exps_cycles_when_alone": float(np.median(len_alone)) if len_alone else None}))
 
 
 def fine_report(tr):
