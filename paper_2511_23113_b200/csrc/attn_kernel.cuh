@@ -144,6 +144,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 domain
 // 3 of 8 (4 of 8 is slower again, profiles/r02_d64_poly_sweep.log); d=128 is
 // smem-port and power bound and only slows down (Wan: 5.71 / 5.97 / 6.32 ms
 // for 0 / 1 / 2 of 8).
+// Which pairs of every 8 go to the FMA pipe: spread out, so the compiler
+// interleaves the polynomial chains with the MUFU stream (3 of 8 at {0,3,5}:
+// 2.94 M vs 2.98 M cycles for {0,1,2} on CogVideoX, tests/variant_cycles.py).
+__host__ __device__ constexpr uint32_t poly_mask(int n) {
+  return n <= 0 ? 0u : n == 1 ? 0x01u : n == 2 ? 0x11u : n == 3 ? 0x29u : n == 4 ? 0x55u : (1u << n) - 1u;
+}
 template <int D>
 __host__ __device__ constexpr int poly_pairs() {
 #ifdef DBSP_POLY_N
@@ -508,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int i = 0; i < 32; ++i) {
             const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
             float2 pp;
-            if ((i & 7) < POLY) {  // FA4-style MUFU offload
+            if ((poly_mask(POLY) >> (i & 7)) & 1) {  // FA4-style MUFU offload
               pp = exp2_poly3_pair(x);
             } else {
               pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
