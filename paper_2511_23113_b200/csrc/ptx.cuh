@@ -54,9 +54,14 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifdef DBSP_WATCHDOG
-  uint32_t spins = 0;
+  // try_wait may suspend for a long, implementation-defined time per call:
+  // bound the wait by %globaltimer (2 s) rather than by a spin count.
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins == (1u << 26)) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 2000000000ull) {
       printf("dbsp watchdog: block %d thread %d stuck on mbarrier 0x%x parity %u\n", blockIdx.x,
              threadIdx.x, bar, parity);
       __trap();

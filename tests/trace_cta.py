@@ -64,6 +64,28 @@ def main():
         "fixed_ns_fit": None,
         "sm_clock_mhz_in_kernel": float(np.median(tr[:, 3] / np.maximum(dur, 1)) * 1e3),
     }
+    # Per SM: time with fewer than 2 resident CTAs (between the first start
+    # and the last end on that SM), and the end -> next start gaps.
+    lows, gaps = [], []
+    for s_id in np.unique(sm):
+        idx = np.where(sm == s_id)[0]
+        ev = sorted([(st[i], 1) for i in idx] + [(en[i], -1) for i in idx])
+        cur, last_t, low = 0, ev[0][0], 0
+        for t, dlt in ev:
+            if cur < 2:
+                low += t - last_t
+            cur += dlt
+            last_t = t
+        lows.append(low / max(1, en[idx].max() - st[idx].min()))
+        ends = np.sort(en[idx])
+        starts = np.sort(st[idx])
+        for e in ends[:-2]:
+            nxt = starts[starts >= e]
+            if len(nxt):
+                gaps.append(nxt[0] - e)
+    res["per_sm_frac_time_below_2_ctas"] = float(np.median(lows))
+    res["cta_turnover_gap_ns_median"] = float(np.median(gaps)) if gaps else None
+    res["cta_turnover_gap_ns_p90"] = float(np.percentile(gaps, 90)) if gaps else None
     A = np.vstack([cnt, np.ones_like(cnt)]).T.astype(np.float64)
     coef, *_ = np.linalg.lstsq(A, dur.astype(np.float64), rcond=None)
     res["fixed_ns_fit"] = {"ns_per_tile": float(coef[0]), "ns_fixed": float(coef[1])}
