@@ -379,6 +379,52 @@ def test_full_size_sampled_rows(name):
     assert np.abs(la[fin] - lr[fin]).max() < 1e-2
 
 
+@pytest.mark.parametrize("name", ["wan", "wan-random", "wan-banded", "cogvideox", "hunyuan", "toy"])
+def test_full_size_every_row_vs_torch_fp32(name):
+    # BASELINE configs B/C/D at full size, EVERY output row: a plain torch
+    # fp32 masked attention (TF32 off) computed on the GPU in 1024-row chunks
+    # from the same block masks (mask.hpp:18-20: tile (q, k) is computed iff
+    # its bit is set).  The CPU oracle pins sampled rows of the same layers in
+    # test_full_size_sampled_rows; this covers the rest.
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    wl = WORKLOADS[name]
+    masks = D.generate_mask_set(wl.spec())
+    H, S, d = wl.heads, wl.tokens, wl.head_dim
+    nq, nk = masks.num_q_blocks, masks.num_kv_blocks
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    out = sparse_attention(q, k, v, masks)
+    torch.cuda.synchronize()
+    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).cuda()  # [H, nq, wpr]
+    shifts = torch.arange(64, device="cuda", dtype=torch.int64)
+    tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        scale = 1.0 / math.sqrt(d)
+        CH = 1024
+        mx, err2, ref2 = 0.0, 0.0, 0.0
+        for h in range(H):
+            bits = ((words[h].unsqueeze(-1) >> shifts) & 1).bool().reshape(nq, -1)[:, :nk]  # [nq, nk]
+            kh, vh = k[:, h].float(), v[:, h].float()
+            for q0 in range(0, S, CH):
+                q1 = min(S, q0 + CH)
+                s = (q[q0:q1, h].float() @ kh.T) * scale
+                m = bits[q0 // 64:(q1 + 63) // 64].repeat_interleave(64, 0)[: q1 - q0]
+                m = m.repeat_interleave(64, 1)[:, :S]
+                s.masked_fill_(~m, float("-inf"))
+                p = torch.softmax(s, dim=-1).nan_to_num_(0.0)  # rows with no keys -> 0
+                ref = p @ vh
+                diff = out[q0:q1, h].float() - ref
+                mx = max(mx, float(diff.abs().max()))
+                err2 += float((diff * diff).sum())
+                ref2 += float((ref * ref).sum())
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+    rel = math.sqrt(err2 / ref2)
+    print(f"every-row parity {name}: max_abs={mx:.3e} rel_l2={rel:.3e} ({H} heads x {S} rows)")
+    assert mx <= MAX_ABS and rel <= REL_L2, f"{name}: every row, max_abs={mx:.3e} rel_l2={rel:.3e}"
+
+
 @pytest.mark.parametrize("strategy", ["U8R1", "U4R2", "U2R4", "U1R8"])
 @pytest.mark.parametrize("balanced", [False, True])
 def test_fused_o_return_matches_separate_exchange(strategy, balanced):
