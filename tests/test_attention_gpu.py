@@ -379,50 +379,76 @@ def test_full_size_sampled_rows(name):
     assert np.abs(la[fin] - lr[fin]).max() < 1e-2
 
 
+def torch_fp32_masked_attention(q, k, v, masks, chunk=1024):
+    """Plain torch fp32 block-masked attention on the GPU (TF32 off), in
+    1024-row chunks: tile (q, k) is computed iff its mask bit is set
+    (mask.hpp:18-20); a row with no keys gives 0.  [S, H, d] float32."""
+    S, H, d = q.shape
+    nq, nk = masks.num_q_blocks, masks.num_kv_blocks
+    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).cuda()  # [H, nq, wpr]
+    shifts = torch.arange(64, device="cuda", dtype=torch.int64)
+    ref = torch.empty(S, H, d, device="cuda", dtype=torch.float32)
+    tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        scale = 1.0 / math.sqrt(d)
+        for h in range(H):
+            bits = ((words[h].unsqueeze(-1) >> shifts) & 1).bool().reshape(nq, -1)[:, :nk]  # [nq, nk]
+            kh, vh = k[:, h].float(), v[:, h].float()
+            for q0 in range(0, S, chunk):
+                q1 = min(S, q0 + chunk)
+                s = (q[q0:q1, h].float() @ kh.T) * scale
+                m = bits[q0 // 64:(q1 + 63) // 64].repeat_interleave(64, 0)[: q1 - q0]
+                s.masked_fill_(~m.repeat_interleave(64, 1)[:, :S], float("-inf"))
+                ref[q0:q1, h] = torch.softmax(s, dim=-1).nan_to_num_(0.0) @ vh
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+    return ref
+
+
+def every_row_error(out, ref):
+    diff = out.float() - ref
+    return float(diff.abs().max()), float(diff.norm() / ref.norm())
+
+
 @pytest.mark.parametrize("name", ["wan", "wan-random", "wan-banded", "cogvideox", "hunyuan", "toy"])
 def test_full_size_every_row_vs_torch_fp32(name):
-    # BASELINE configs B/C/D at full size, EVERY output row: a plain torch
-    # fp32 masked attention (TF32 off) computed on the GPU in 1024-row chunks
-    # from the same block masks (mask.hpp:18-20: tile (q, k) is computed iff
-    # its bit is set).  The CPU oracle pins sampled rows of the same layers in
+    # BASELINE configs B/C/D at full size, EVERY output row, against a plain
+    # torch fp32 masked attention computed on the GPU from the same block
+    # masks.  The CPU oracle pins sampled rows of the same layers in
     # test_full_size_sampled_rows; this covers the rest.
     from paper_2511_23113_b200.workloads import WORKLOADS
     wl = WORKLOADS[name]
     masks = D.generate_mask_set(wl.spec())
     H, S, d = wl.heads, wl.tokens, wl.head_dim
-    nq, nk = masks.num_q_blocks, masks.num_kv_blocks
     g = torch.Generator(device="cuda").manual_seed(7)
     q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
     out = sparse_attention(q, k, v, masks)
-    torch.cuda.synchronize()
-    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).cuda()  # [H, nq, wpr]
-    shifts = torch.arange(64, device="cuda", dtype=torch.int64)
-    tf32 = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        scale = 1.0 / math.sqrt(d)
-        CH = 1024
-        mx, err2, ref2 = 0.0, 0.0, 0.0
-        for h in range(H):
-            bits = ((words[h].unsqueeze(-1) >> shifts) & 1).bool().reshape(nq, -1)[:, :nk]  # [nq, nk]
-            kh, vh = k[:, h].float(), v[:, h].float()
-            for q0 in range(0, S, CH):
-                q1 = min(S, q0 + CH)
-                s = (q[q0:q1, h].float() @ kh.T) * scale
-                m = bits[q0 // 64:(q1 + 63) // 64].repeat_interleave(64, 0)[: q1 - q0]
-                m = m.repeat_interleave(64, 1)[:, :S]
-                s.masked_fill_(~m, float("-inf"))
-                p = torch.softmax(s, dim=-1).nan_to_num_(0.0)  # rows with no keys -> 0
-                ref = p @ vh
-                diff = out[q0:q1, h].float() - ref
-                mx = max(mx, float(diff.abs().max()))
-                err2 += float((diff * diff).sum())
-                ref2 += float((ref * ref).sum())
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = tf32
-    rel = math.sqrt(err2 / ref2)
+    mx, rel = every_row_error(out, torch_fp32_masked_attention(q, k, v, masks))
     print(f"every-row parity {name}: max_abs={mx:.3e} rel_l2={rel:.3e} ({H} heads x {S} rows)")
     assert mx <= MAX_ABS and rel <= REL_L2, f"{name}: every row, max_abs={mx:.3e} rel_l2={rel:.3e}"
+
+
+def test_full_size_sp_splits_every_row_vs_torch_fp32():
+    # The Wan layer executed as every G=8 U x R split, uniform (USP default
+    # plan) and db-SP (plan_dual), each rank's per-period kernels with the
+    # ring accumulate/finalize merge, run on one GPU (simulate_on_one_gpu):
+    # every output row against the torch fp32 reference.
+    from paper_2511_23113_b200.sp import simulate_on_one_gpu
+    from paper_2511_23113_b200.workloads import WORKLOADS
+    wl = WORKLOADS["wan"]
+    masks = D.generate_mask_set(wl.spec())
+    H, S, d = wl.heads, wl.tokens, wl.head_dim
+    g = torch.Generator(device="cuda").manual_seed(8)
+    q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    ref = torch_fp32_masked_attention(q, k, v, masks)
+    for strategy in ("U8R1", "U4R2", "U2R4", "U1R8"):
+        st = D.parse_strategy(strategy)
+        for bal, plan in (("uniform", D.default_plan(masks, st)), ("dbsp", D.plan_dual(masks, st).plan)):
+            out, _ = simulate_on_one_gpu(q, k, v, masks, st, plan, time_kernels=False)
+            mx, rel = every_row_error(out, ref)
+            print(f"every-row parity wan {strategy}/{bal}: max_abs={mx:.3e} rel_l2={rel:.3e}")
+            assert mx <= MAX_ABS and rel <= REL_L2, f"{strategy}/{bal}: max_abs={mx:.3e} rel_l2={rel:.3e}"
 
 
 @pytest.mark.parametrize("strategy", ["U8R1", "U4R2", "U2R4", "U1R8"])
