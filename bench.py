@@ -376,6 +376,8 @@ def sp_projection(q, k, v, masks, G: int = 8) -> dict:
     from paper_2511_23113_b200.attention import sparse_attention
     from paper_2511_23113_b200.sp import measured_rho, simulate_on_one_gpu
 
+    from paper_2511_23113_b200.sp_bench import load_profile, profile_comm_source, profile_path
+    prof = load_profile("wan")
     ref = sparse_attention(q, k, v, masks)
     out = {}
     for st in D.enumerate_strategies(G):
@@ -385,17 +387,32 @@ def sp_projection(q, k, v, masks, G: int = 8) -> dict:
             o, t = simulate_on_one_gpu(q, k, v, masks, st, plan)
             crit = float(sum(max(row) for row in t))
             err = float((o.float() - ref.float()).abs().max())
+            # Eq. 4 communication of the same plan (latency.hpp:225-268): the
+            # Ulysses all-to-all, the ring p2p not hidden behind compute and
+            # the balancing exchange, from the B200 profile.
+            lat = D.predict_latency(masks, st, plan, prof)
+            comm_ms = (lat.all2all_s + lat.ring_p2p_exposed_s + lat.exchange_s) * 1e3
             out[f"{st}/{name}"] = {"attn_critical_path_ms": round(crit, 4),
+                                   "comm_modelled_ms": round(comm_ms, 4),
+                                   "layer_ms_with_modelled_comm": round(crit + comm_ms, 4),
                                    "rho_s_measured": round(measured_rho(t), 4),
                                    "rho_s_plan": round(D.imbalance_ratio(D.workload_table(masks, st, plan)), 4),
                                    "max_abs_vs_single_gpu": round(err, 5)}
     planning = planning_on_critical_path(q, k, v, masks, G)
-    best_uniform = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("uniform"))
-    best_dbsp = min(v["attn_critical_path_ms"] for k_, v in out.items() if k_.endswith("dbsp"))
+
+    def best(suffix, key):
+        return min(v[key] for k_, v in out.items() if k_.endswith(suffix))
+    best_uniform, best_dbsp = best("uniform", "attn_critical_path_ms"), best("dbsp", "attn_critical_path_ms")
+    bu_c, bd_c = best("uniform", "layer_ms_with_modelled_comm"), best("dbsp", "layer_ms_with_modelled_comm")
     return {"gpus_simulated": G, "splits": out, "best_uniform_ms": best_uniform, "best_dbsp_ms": best_dbsp,
             "speedup_dbsp_vs_best_uniform": round(best_uniform / best_dbsp, 4),
+            "best_uniform_ms_with_modelled_comm": bu_c, "best_dbsp_ms_with_modelled_comm": bd_c,
+            "speedup_dbsp_vs_best_uniform_with_modelled_comm": round(bu_c / bd_c, 4),
+            "comm_profile": f"{profile_path('wan').name} (comm curves {profile_comm_source('wan')})",
             "planning_on_critical_path": planning,
-            "note": "per-rank kernels measured on one B200; communication not included"}
+            "note": "per-rank kernels measured on one B200 (median of 5 launches each); communication: "
+                    "attention-only figures exclude it, the *_with_modelled_comm ones add the Eq. 4 terms "
+                    "of the B200 profile (nominal NVLink curves until the NCCL sweep runs on >1 GPU)"}
 
 
 def planning_on_critical_path(q, k, v, masks, G: int = 8, calls: int = 20) -> dict:

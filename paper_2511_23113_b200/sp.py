@@ -360,7 +360,7 @@ def scatter_maps(layout: RankLayout, world: int, nb: int, tokens: int):
 
 # ----------------------------------------------------------------------------- single-GPU simulation
 def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStrategy, plan: PartitionPlan,
-                        time_kernels: bool = True, reps: int = 3, fuse_return: bool = False):
+                        time_kernels: bool = True, reps: int = 5, fuse_return: bool = False):
     """Run every rank's per-period kernels of UxRy on ONE GPU (no exchange:
     the local buffers are gathered from the global tensors), merge exactly as
     the distributed path does, and time each (rank, period) launch with CUDA
@@ -368,7 +368,7 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
     G separate home-shard buffers through the kernel's scatter epilogue (the
     fused reverse all-to-all; on one GPU the "peers" are local allocations),
     and the result is their concatenation.  Returns (out [S,H,d],
-    times_ms[period][rank])."""
+    times_ms[period][rank]); each time is the median of `reps` launches."""
     import torch
     from .attention import AttentionSchedule, OutScatter, accum_init
 
@@ -418,7 +418,7 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
                 oa = torch.empty_like(o_acc)
                 la = torch.empty_like(lse_acc)
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                best = float("inf")
+                samples = []
                 for _ in range(reps):
                     accum_init(oa, la)
                     ev[0].record()
@@ -428,8 +428,8 @@ def simulate_on_one_gpu(q, k, v, masks: AttentionMaskSet, strategy: ParallelStra
                         sc.launch(q_loc, k_loc, v_loc, o_loc, o_accum=oa, lse_accum=la, accumulate=True)
                     ev[1].record()
                     torch.cuda.synchronize()
-                    best = min(best, ev[0].elapsed_time(ev[1]))
-                times[p][lay.rank] = best
+                    samples.append(ev[0].elapsed_time(ev[1]))
+                times[p][lay.rank] = float(np.median(samples))  # median: not the best-clock sample
             last = p == y - 1
             sk = scat if last else None
             if y == 1:
