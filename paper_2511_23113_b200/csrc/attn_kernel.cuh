@@ -169,14 +169,10 @@ struct KCfg {
   // room for only one S buffer next to the 128-col O, which serialises
   // softmax and MMA inside a CTA (measured 1.24x slower than Q in smem with
   // two S buffers), so Q stays in smem (SS-mode QK^T) there.
-#ifdef DBSP_D64_QSMEM3
-  // d=64 alternative: Q in smem frees 32 TMEM columns for a third S buffer.
-  static constexpr bool kQInTmem = false;
-  static constexpr int kNSB = D == 64 ? 3 : 2;
-#else
+  // (Round 1 also measured d=64 with Q in smem and a third S buffer in the
+  // freed columns: within 1% -- profiles/r01_k4_analysis.md.)
   static constexpr bool kQInTmem = D == 64;
   static constexpr int kNSB = 2;
-#endif
   static constexpr uint32_t kQBytes = kQInTmem ? 0u : 128u * D * 2u;
   static constexpr uint32_t kQChunk = 128u * 128u;  // one 64-column chunk of a 128-row Q tile
   // TMEM columns (256 per CTA): [Q], NSB S/P buffers of 64 cols, O (fp32, D
@@ -428,12 +424,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // global load of entry j would otherwise sit on the softmax chain.
     uint32_t e_next = count > 0 ? __ldg(ent) : 0u;
     for (uint32_t j = 0; j < count; ++j) {
-#ifndef DBSP_NO_ENTRY_PREFETCH
       const uint32_t e = e_next;
       if (j + 1 < count) e_next = __ldg(ent + j + 1);
-#else
-      const uint32_t e = __ldg(ent + j);
-#endif
       const bool dense = (e & dense_bit) != 0;  // warp-uniform (one half per warp)
       const int b = int(j % NSB);
       const uint32_t scol = tmem + lane_off + C::kColS + 64u * b;
