@@ -22,8 +22,8 @@ void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Sched
   flags = normalize_sched_flags(flags);
   const bool pair_q = (flags & kSchedPairQ) != 0;
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
-  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto: K/V of <= 8 heads x 512 blocks
-    global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
+  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto (schedule.hpp)
+    global_lpt = uint64_t(v.heads) * v.kv_blocks <= kGlobalLptMaxHeadBlocks;
   if (v.heads == 0 || v.q_blocks == 0 || v.kv_blocks == 0)
     fail(kConfig, "local view dimensions must be positive");
   if (v.kv_blocks > kEntryKvMask) fail(kConfig, "too many local KV blocks");

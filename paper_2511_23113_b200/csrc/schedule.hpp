@@ -54,6 +54,16 @@ struct Schedule {
 constexpr uint32_t kSchedPairQ = 1;      // two Q blocks per 128-row tile
 constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all heads
 constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
+// Neither bit set: global LPT when local heads x KV blocks <= this, else per
+// head (K/V of one head at a time stays in L2).  Measured on one B200 with
+// 30 back-to-back launches per variant (tests/ab_probe.py --sustained, flags
+// 1|4 vs 1|2): global order wins on CogVideoX (48 x 278 = 13,344: 1.71 vs
+// 1.86 ms) -- the heaviest items of every head start first, the tail is the
+// shortest items -- but loses on Wan (40 x 512 = 20,480: 6.30 vs 5.97 ms) and
+// HunyuanVideo (24 x 1857), whose K/V (0.67 / 1.46 GB) then misses the 126 MB
+// L2 more and, power-capped, runs at a lower clock.  (Short bursts of
+// launches favour global order on Wan too; the bench's sustained steps do not.)
+constexpr uint64_t kGlobalLptMaxHeadBlocks = 16384;
 constexpr uint32_t kSchedQuad = 8;       // layout: four Q blocks per item
 constexpr uint32_t kSchedKey128 = 16;    // layout: 128-key steps
 constexpr uint32_t kSchedCtaPair = 128;  // d=128 CTA-pair kernel (attn_kernel_pd3.cuh); implies 1|8|16

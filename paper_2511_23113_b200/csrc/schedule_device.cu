@@ -254,7 +254,8 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
            const uint64_t* d_present, const int32_t* d_kv_local, dbsp_core::WorkItem* items_out,
            uint32_t* entries_out, void*& scratch, size_t& scratch_bytes, cudaStream_t stream) {
   bool global_lpt = (flags & kSchedGlobalLpt) != 0;
-  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder))) global_lpt = uint64_t(v.heads) * v.kv_blocks <= 4096;
+  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto (schedule.hpp)
+    global_lpt = uint64_t(v.heads) * v.kv_blocks <= kGlobalLptMaxHeadBlocks;
   const uint32_t step = (flags & kSchedQuad) ? 4 : (flags & kSchedPairQ) ? 2 : 1;
   const uint32_t per_head = (v.q_blocks + step - 1) / step;
   const uint32_t n = v.heads * per_head;

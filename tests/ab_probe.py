@@ -19,6 +19,11 @@ from paper_2511_23113_b200.workloads import WORKLOADS  # noqa: E402
 def main():
     args = sys.argv[1:]
     rounds = 5
+    per_round = 8
+    if "--sustained" in args:  # 30 back-to-back launches per variant and round, median of the last 20
+        i = args.index("--sustained")
+        args = args[:i] + args[i + 1:]
+        per_round = 30
     if "--rounds" in args:
         i = args.index("--rounds")
         rounds = int(args[i + 1])
@@ -44,14 +49,14 @@ def main():
     for _ in range(rounds):
         for f, sc in zip(flag_list, scheds):
             ts = []
-            for _ in range(8):
+            for _ in range(per_round):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 sc.launch(q, k, v, o)
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
-            res[f].append(float(np.median(ts)))
+            res[f].append(float(np.median(ts[-20:] if per_round > 20 else ts)))
     out = {"workload": wl.name}
     for f in flag_list:
         r = np.array(res[f])

@@ -1,7 +1,8 @@
 """Cycles per K4 launch for kernel variants chosen by an environment switch
 (e.g. DBSP_K4_VAR), measured by ncu (gpu__time_duration, sm cycles) over N
 launches each, medians -- steadier than wall-clock A/B under the power cap.
-GPU-box tool: python tests/variant_cycles.py workload VAR v1 v2 ... [--n N]."""
+GPU-box tool: python tests/variant_cycles.py workload VAR v1 v2 ... [--n N]
+(VAR FLAGS compares schedule flag words instead of an environment switch)."""
 import csv
 import io
 import json
@@ -16,10 +17,12 @@ METRICS = "gpu__time_duration.sum,sm__cycles_elapsed.avg,smsp__inst_executed.sum
 
 
 def run(workload, var, val, n):
-    env = dict(os.environ, **{var: val, "DBSP_PROBE_N": str(n)})
+    # var FLAGS: `val` is the schedule flags word passed to k4_one_probe.py
+    env = dict(os.environ, DBSP_PROBE_N=str(n), **({} if var == "FLAGS" else {var: val}))
+    flags = val if var == "FLAGS" else "1"
     out = subprocess.run(["ncu", "--csv", "--metrics", METRICS, "--clock-control", "none",
                           "-k", "regex:sparse_attn_fwd", sys.executable, str(ROOT / "tests" / "k4_one_probe.py"),
-                          "1", workload], env=env, capture_output=True, text=True, timeout=900)
+                          flags, workload], env=env, capture_output=True, text=True, timeout=900)
     lines = [l for l in out.stdout.splitlines() if l.startswith('"')]
     rows = list(csv.DictReader(io.StringIO("\n".join(lines))))
     per = {}
