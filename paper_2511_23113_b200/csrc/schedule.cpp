@@ -21,9 +21,7 @@ uint32_t normalize_sched_flags(uint32_t flags) {
 void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Schedule& out) {
   flags = normalize_sched_flags(flags);
   const bool pair_q = (flags & kSchedPairQ) != 0;
-  bool global_lpt = (flags & kSchedGlobalLpt) != 0;
-  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto (schedule.hpp)
-    global_lpt = uint64_t(v.heads) * v.kv_blocks <= kGlobalLptMaxHeadBlocks;
+  const uint32_t head_group = lpt_head_group(flags, v.heads, v.kv_blocks);  // 0 = global LPT
   if (v.heads == 0 || v.q_blocks == 0 || v.kv_blocks == 0)
     fail(kConfig, "local view dimensions must be positive");
   if (v.kv_blocks > kEntryKvMask) fail(kConfig, "too many local KV blocks");
@@ -130,12 +128,13 @@ void build_schedule(const MaskView& m, const LocalView& v, uint32_t flags, Sched
   std::vector<uint32_t> order(raw.size());
   std::iota(order.begin(), order.end(), 0u);
   // Heaviest-first (LPT) launch order.  The hardware hands CTAs to free SM
-  // slots in blockIdx order, so this is a dynamic LPT schedule.  For large
-  // problems the order is per head so concurrently running CTAs share a
-  // head's K/V in L2; when the whole local K/V fits comfortably in L2 the
-  // order is global, which removes the per-head tails.
+  // slots in blockIdx order, so this is a dynamic LPT schedule, within head
+  // groups whose K/V fits the L2 (schedule.hpp lpt_head_group).
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
-    if (!global_lpt && raw[x].it.head != raw[y].it.head) return raw[x].it.head < raw[y].it.head;
+    if (head_group) {
+      const uint32_t gx = raw[x].it.head / head_group, gy = raw[y].it.head / head_group;
+      if (gx != gy) return gx < gy;
+    }
     return raw[x].it.count > raw[y].it.count;
   });
   out.items.clear();

@@ -54,16 +54,26 @@ struct Schedule {
 constexpr uint32_t kSchedPairQ = 1;      // two Q blocks per 128-row tile
 constexpr uint32_t kSchedGlobalLpt = 2;  // heaviest items first across all heads
 constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, heads in order
-// Neither bit set: global LPT when local heads x KV blocks <= this, else per
-// head (K/V of one head at a time stays in L2).  Measured on one B200 with
-// 30 back-to-back launches per variant (tests/ab_probe.py --sustained, flags
-// 1|4 vs 1|2): global order wins on CogVideoX (48 x 278 = 13,344: 1.71 vs
-// 1.86 ms) -- the heaviest items of every head start first, the tail is the
-// shortest items -- but loses on Wan (40 x 512 = 20,480: 6.30 vs 5.97 ms) and
-// HunyuanVideo (24 x 1857), whose K/V (0.67 / 1.46 GB) then misses the 126 MB
-// L2 more and, power-capped, runs at a lower clock.  (Short bursts of
-// launches favour global order on Wan too; the bench's sustained steps do not.)
-constexpr uint64_t kGlobalLptMaxHeadBlocks = 16384;
+// Neither bit set: heads in groups of max(1, kLptGroupKvBlocks / local KV
+// blocks) -- a group's K/V (at d=128: 2048 blocks x 64 keys x 128 x 2 B x
+// (K, V) = 64 MB) fits the 126 MB L2 -- heaviest-first within each group,
+// groups in head order.  Measured on one B200 (tests/ab_probe.py --sustained,
+// 30 back-to-back launches per variant; tests/variant_cycles.py for DRAM):
+//   CogVideoX (48 heads x 278 blocks, groups of 7): 1.72 ms vs 1.76 global
+//     LPT (1.94 GB DRAM per launch) vs 1.91 per-head (0.42 GB); 0.42 GB;
+//   Wan (40 x 512, groups of 4): 6.006 vs 6.004 ms per-head vs 6.42 global
+//     (6.4 GB DRAM: power-capped, it costs clock);
+//   HunyuanVideo (24 x 1857): groups of 1 = per-head.
+// Global order starts every head's heaviest items first; a group keeps that
+// across the group's heads while its K/V stays in L2.
+constexpr uint32_t kLptGroupKvBlocks = 2048;
+// Heads per ordering group for a local view (0 = one group: global LPT).
+inline uint32_t lpt_head_group(uint32_t flags, uint32_t heads, uint32_t kv_blocks) {
+  if (flags & kSchedGlobalLpt) return 0;
+  if (flags & kSchedHeadOrder) return 1;
+  const uint32_t g = kLptGroupKvBlocks / (kv_blocks ? kv_blocks : 1u);
+  return g >= heads ? 0u : (g ? g : 1u);
+}
 constexpr uint32_t kSchedQuad = 8;       // layout: four Q blocks per item
 constexpr uint32_t kSchedKey128 = 16;    // layout: 128-key steps
 constexpr uint32_t kSchedCtaPair = 128;  // d=128 CTA-pair kernel (attn_kernel_pd3.cuh); implies 1|8|16

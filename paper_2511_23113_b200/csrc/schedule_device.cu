@@ -36,7 +36,7 @@ struct K2Args {
   uint32_t kv_tokens_global;  // 0 = all blocks full
   uint32_t items_per_head;
   uint32_t step;              // 1, 2 (paired Q blocks) or 4 (quad items of the CTA-pair kernel)
-  uint32_t head_order;        // 1 = per-head LPT, 0 = global LPT
+  uint32_t head_group;        // heads per ordering group; 0 = global LPT (schedule.hpp)
 };
 
 // The Q rows of item i (schedule.cpp): local head, up to four local Q blocks
@@ -80,7 +80,7 @@ __global__ void k2_count(K2Args a, uint32_t n_items, uint32_t* counts, unsigned 
     c += __popcll(uni);
   }
   counts[i] = c;
-  const unsigned long long head_key = a.head_order ? (unsigned long long)r.hl : 0ull;
+  const unsigned long long head_key = a.head_group ? (unsigned long long)(r.hl / a.head_group) : 0ull;
   if (keys) keys[i] = (head_key << 44) | ((unsigned long long)(0xFFFFFu - min(c, 0xFFFFFu)) << 24) | i;
 }
 
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kK2Threads, 1)
     keys[s] = 0xFFFFFFFFu;  // padding sorts last
     if (i < n_items) {
       const uint32_t hl = i / a.items_per_head;
-      keys[s] = ((a.head_order ? hl : 0u) << 22) | (0x3FFFFFu - counts[i]);  // counts < 2^22
+      keys[s] = ((a.head_group ? hl / a.head_group : 0u) << 22) | (0x3FFFFFu - counts[i]);  // counts < 2^22
     }
   }
   K2Sort(sm.sort).Sort(keys, idx, 0, int(key_bits));
@@ -253,17 +253,16 @@ void build(const uint64_t* d_words, uint32_t nq_global, uint32_t nk_global, cons
            uint32_t flags, const uint32_t* d_head_ids, const uint32_t* d_q_ids,
            const uint64_t* d_present, const int32_t* d_kv_local, dbsp_core::WorkItem* items_out,
            uint32_t* entries_out, void*& scratch, size_t& scratch_bytes, cudaStream_t stream) {
-  bool global_lpt = (flags & kSchedGlobalLpt) != 0;
-  if (!(flags & (kSchedGlobalLpt | kSchedHeadOrder)))  // auto (schedule.hpp)
-    global_lpt = uint64_t(v.heads) * v.kv_blocks <= kGlobalLptMaxHeadBlocks;
+  const uint32_t head_group = lpt_head_group(flags, v.heads, v.kv_blocks);  // 0 = global LPT
   const uint32_t step = (flags & kSchedQuad) ? 4 : (flags & kSchedPairQ) ? 2 : 1;
   const uint32_t per_head = (v.q_blocks + step - 1) / step;
   const uint32_t n = v.heads * per_head;
   if (n >= (1u << 24)) fail(kConfig, "too many work items for the device schedule builder");
   dbsp_dev::K2Args a{d_words, nq_global, (nk_global + 63) / 64, d_head_ids, d_q_ids, v.q_blocks,
                      d_present, d_kv_local, v.kv_tokens_global, per_head, step,
-                     global_lpt ? 0u : 1u};
-  const uint32_t head_bits = global_lpt ? 0u : uint32_t(32 - __builtin_clz(std::max(v.heads, 2u) - 1));
+                     head_group};
+  const uint32_t n_groups = head_group ? (v.heads + head_group - 1) / head_group : 1u;
+  const uint32_t head_bits = head_group ? uint32_t(32 - __builtin_clz(std::max(n_groups, 2u) - 1)) : 0u;
   if (n <= uint32_t(dbsp_dev::kFusedItems) && 22 + head_bits <= 32) {
     // one-CTA planner + the entry writer (3 launches)
     const size_t need = 3 * size_t(n) * 4 + 256;
