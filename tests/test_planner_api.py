@@ -416,3 +416,30 @@ def test_auto_d128_schedule_choice():
         quad = AttentionSchedule().build(m, flags=1 | 8 | 16 | 128)
         assert quad.layout()["q_blocks_per_item"] == 4 and quad.stats()["items"] == H * (nb // 4)
         assert AttentionSchedule().build(m, head_dim=64).stats()["items"] == H * (nb // 2)
+
+
+@pytest.mark.parametrize("H,nb,group", [(16, 278, 7), (6, 278, 0), (8, 512, 4), (3, 1857, 1), (4, 64, 0)])
+def test_launch_order_lpt_within_l2_sized_head_groups(H, nb, group):
+    # schedule.hpp lpt_head_group: heads in groups of max(1, 2048 / KV blocks)
+    # (0 = a single group: global LPT), heaviest item first within a group,
+    # groups in head order.  Explicit GLOBAL_LPT / HEAD_ORDER override it.
+    from paper_2511_23113_b200.attention import AttentionSchedule
+    m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 3))
+
+    def order(flags):
+        items, _ = AttentionSchedule().build(m, flags=flags).download()
+        return items[:, 0].astype(np.int64), items[:, 4].astype(np.int64)  # head, count
+
+    def check_groups(heads, counts, g):
+        key = heads // g if g else np.zeros_like(heads)
+        assert np.all(np.diff(key) >= 0), "groups out of head order"
+        for k in np.unique(key):
+            c = counts[key == k]
+            assert np.all(np.diff(c) <= 0), "not heaviest-first within a group"
+
+    heads, counts = order(1)
+    g = 2048 // nb
+    assert (0 if g >= H else max(g, 1)) == group
+    check_groups(heads, counts, group)
+    check_groups(*order(1 | 2), 0)  # GLOBAL_LPT
+    check_groups(*order(1 | 4), 1)  # HEAD_ORDER
