@@ -69,6 +69,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) softmax_kernel(int iters, float
     for (int i = 0; i < 32; ++i) {
       const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
       float2 pp;
+      if constexpr (PACK == 2) {  // packed f16x2 ex2: cvt f32x2 -> f16x2, one MUFU for two exps
+        uint32_t h, e;
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x.y), "f"(x.x));
+        asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+        pk[i] = e;
+        continue;
+      }
       if ((poly_mask(PN) >> (i & 7)) & 1)
         pp = exp2_poly3_pair(x);
       else
@@ -174,13 +181,14 @@ void run() {
   // One 128x64 tile = 4 warp-steps; SM throughput in tiles per cycle:
   const double sm_cycles_per_tile = per_step * 4.0 / WARPS;
   std::printf("poly %d/8 %s warps/SM=%2d (per SMSP %d): %7.1f cycles per warp-step, %7.1f SM cycles per 128x64 tile  %s\n",
-              PN, PACK ? "prmt pack " : NOSUM ? "no row sum" : "row sum   ", WARPS, WARPS / 4, per_step, sm_cycles_per_tile,
+              PN, PACK == 2 ? "f16x2 ex2 " : PACK ? "prmt pack " : NOSUM ? "no row sum" : "row sum   ", WARPS, WARPS / 4, per_step, sm_cycles_per_tile,
               cudaGetErrorString(err));
   cudaFree(d);
   cudaFree(sink);
 }
 
 int main() {
+  // exp pairs on the FMA pipe: 0, 2, 3, 4 of 8, at 2 and 4 softmax warps per SMSP
   run<8, false, 0, 0>();
   run<16, false, 0, 0>();
   run<8, false, 0, 2>();
@@ -189,6 +197,10 @@ int main() {
   run<16, false, 0, 3>();
   run<8, false, 0, 4>();
   run<16, false, 0, 4>();
+  run<8, true>();           // no row sum
+  run<8, false, 1>();       // bf16 by byte permute instead of F2FP
+  run<8, false, 2, 0>();    // ex2.approx.f16x2 (two exps per MUFU op)
+  run<16, false, 2, 0>();
   run_ld<8>();
   return 0;
 }
