@@ -627,3 +627,32 @@ def test_fused_scatter_every_d128_kernel(flags):
     for b in range(nb):
         got = homes[b % 2][(b // 2) * 64:(b // 2 + 1) * 64].flip(1)
         assert torch.equal(got, ref[b * 64:(b + 1) * 64]), f"flags {flags} block {b}"
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("pattern", ["clustered", "random"])
+def test_matches_flashinfer_block_sparse(d, pattern):
+    # An independent implementation of the same block-sparse semantics:
+    # FlashInfer's VariableBlockSparseAttentionWrapper with the per-head 64x64
+    # block maps (library code, used here only as a second checker).  Rows that
+    # see at least one key are compared (FlashInfer leaves empty rows undefined).
+    fi = pytest.importorskip("flashinfer")
+    H, S = 8, 4096
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, pattern, 0.15, 0.45, 1.0, 5))
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(S, H, d, device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    out = sparse_attention(q, k, v, masks)
+    words = torch.from_numpy(np.ascontiguousarray(masks.words).view(np.int64)).cuda()
+    bits = ((words.unsqueeze(-1) >> torch.arange(64, device="cuda")) & 1).bool().reshape(H, nb, -1)[:, :, :nb]
+    w = fi.VariableBlockSparseAttentionWrapper(torch.empty(128 << 20, dtype=torch.uint8, device="cuda"))
+    w.plan(bits.contiguous(), torch.full((H, nb), 64, dtype=torch.int32, device="cuda"),
+           torch.full((H, nb), 64, dtype=torch.int32, device="cuda"), H, H, d,
+           q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
+    ref = w.run(*(t.transpose(0, 1).contiguous() for t in (q, k, v)))
+    if ref.shape[0] == H:
+        ref = ref.transpose(0, 1)
+    sel = bits.any(dim=-1).transpose(0, 1).repeat_interleave(64, 0)[:S]  # [S, H]
+    diff = out.float()[sel] - ref.float()[sel]
+    mx, rel = float(diff.abs().max()), float(diff.norm() / ref.float()[sel].norm())
+    assert mx <= MAX_ABS and rel <= REL_L2, f"d={d} {pattern}: max_abs={mx:.3e} rel_l2={rel:.3e}"
