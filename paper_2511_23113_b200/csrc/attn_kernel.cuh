@@ -423,6 +423,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     // Entries are read one step ahead: when S_j is already waiting, the
     // global load of entry j would otherwise sit on the softmax chain.
     uint32_t e_next = count > 0 ? __ldg(ent) : 0u;
+    // Unrolled by the S-buffer count: 2% fewer instructions (buffer index and
+    // phase become constants), CogVideoX 2.804 M vs 2.821 M cycles (ncu).
+#pragma unroll 2
     for (uint32_t j = 0; j < count; ++j) {
       const uint32_t e = e_next;
       if (j + 1 < count) e_next = __ldg(ent + j + 1);
