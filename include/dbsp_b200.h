@@ -333,7 +333,8 @@ void dbsp_schedule_destroy(dbsp_schedule* sched);
  * M=128 path).  Launch order is heaviest-first; GLOBAL_LPT orders across
  * heads, HEAD_ORDER within each head (K/V of concurrently running CTAs stays
  * L2-resident); with neither, heaviest-first within groups of
- * max(1, 2048 / local KV blocks) heads (a group's K/V fits the L2). */
+ * max(1, 2048 / local KV blocks) heads (a group's K/V fits the L2), one group
+ * for views of <= 4096 head x KV blocks. */
 enum { DBSP_SCHED_PAIR_Q = 1, DBSP_SCHED_GLOBAL_LPT = 2, DBSP_SCHED_HEAD_ORDER = 4,
        DBSP_SCHED_QUAD = 8 /* layout bit: 4 Q blocks per item (set by CTA_PAIR) */,
        DBSP_SCHED_KEY128 = 16 /* layout bit: 128-key steps (set by CTA_PAIR) */,

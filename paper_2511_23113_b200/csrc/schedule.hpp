@@ -67,10 +67,16 @@ constexpr uint32_t kSchedHeadOrder = 4;  // heaviest first within each head, hea
 // Global order starts every head's heaviest items first; a group keeps that
 // across the group's heads while its K/V stays in L2.
 constexpr uint32_t kLptGroupKvBlocks = 2048;
+// Small views (a few waves of CTAs, e.g. one SP rank's share) stay one group:
+// a last head group would otherwise run as a serial tail (the G=8 Wan
+// per-rank kernels -- 5 heads x 512 blocks -- measured 1.26x instead of 1.41x
+// db-SP over uniform when split into groups of 4 + 1).
+constexpr uint64_t kLptGroupMinHeadBlocks = 4096;
 // Heads per ordering group for a local view (0 = one group: global LPT).
 inline uint32_t lpt_head_group(uint32_t flags, uint32_t heads, uint32_t kv_blocks) {
   if (flags & kSchedGlobalLpt) return 0;
   if (flags & kSchedHeadOrder) return 1;
+  if (uint64_t(heads) * kv_blocks <= kLptGroupMinHeadBlocks) return 0;
   const uint32_t g = kLptGroupKvBlocks / (kv_blocks ? kv_blocks : 1u);
   return g >= heads ? 0u : (g ? g : 1u);
 }

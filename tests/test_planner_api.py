@@ -418,10 +418,11 @@ def test_auto_d128_schedule_choice():
         assert AttentionSchedule().build(m, head_dim=64).stats()["items"] == H * (nb // 2)
 
 
-@pytest.mark.parametrize("H,nb,group", [(16, 278, 7), (6, 278, 0), (8, 512, 4), (3, 1857, 1), (4, 64, 0)])
+@pytest.mark.parametrize("H,nb,group", [(16, 278, 7), (6, 278, 0), (9, 512, 4), (5, 512, 0), (3, 1857, 1), (4, 64, 0)])
 def test_launch_order_lpt_within_l2_sized_head_groups(H, nb, group):
     # schedule.hpp lpt_head_group: heads in groups of max(1, 2048 / KV blocks)
-    # (0 = a single group: global LPT), heaviest item first within a group,
+    # (0 = a single group: global LPT, also for views of <= 4096 head x KV
+    # blocks), heaviest item first within a group,
     # groups in head order.  Explicit GLOBAL_LPT / HEAD_ORDER override it.
     from paper_2511_23113_b200.attention import AttentionSchedule
     m = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.15, 0.45, 1.0, 3))
@@ -439,7 +440,7 @@ def test_launch_order_lpt_within_l2_sized_head_groups(H, nb, group):
 
     heads, counts = order(1)
     g = 2048 // nb
-    assert (0 if g >= H else max(g, 1)) == group
+    assert (0 if (H * nb <= 4096 or g >= H) else max(g, 1)) == group
     check_groups(heads, counts, group)
     check_groups(*order(1 | 2), 0)  # GLOBAL_LPT
     check_groups(*order(1 | 4), 1)  # HEAD_ORDER
