@@ -2,7 +2,8 @@
 (e.g. DBSP_K4_VAR), measured by ncu (gpu__time_duration, sm cycles) over N
 launches each, medians -- steadier than wall-clock A/B under the power cap.
 GPU-box tool: python tests/variant_cycles.py workload VAR v1 v2 ... [--n N]
-(VAR FLAGS compares schedule flag words instead of an environment switch)."""
+(VAR FLAGS compares schedule flag words instead of an environment switch; otherwise
+DBSP_PROBE_FLAGS, default 1, is the flags word)."""
 import csv
 import io
 import json
@@ -20,7 +21,7 @@ METRICS = ("gpu__time_duration.sum,sm__cycles_elapsed.avg,smsp__inst_executed.su
 def run(workload, var, val, n):
     # var FLAGS: `val` is the schedule flags word passed to k4_one_probe.py
     env = dict(os.environ, DBSP_PROBE_N=str(n), **({} if var == "FLAGS" else {var: val}))
-    flags = val if var == "FLAGS" else "1"
+    flags = val if var == "FLAGS" else os.environ.get("DBSP_PROBE_FLAGS", "1")
     out = subprocess.run(["ncu", "--csv", "--metrics", METRICS, "--clock-control", "none", "--cache-control", "none",
                           "-k", "regex:sparse_attn_fwd", sys.executable, str(ROOT / "tests" / "k4_one_probe.py"),
                           flags, workload], env=env, capture_output=True, text=True, timeout=900)
