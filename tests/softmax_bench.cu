@@ -60,7 +60,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) softmax_kernel(int iters, float
     }
     const float mt2 =
         fmaxf(fmax3f(mx[0], mx[1], mx[2]), fmax3f(fmax3f(mx[3], mx[4], mx[5]), mx[6], mx[7])) * scale_log2;
-    if (mt2 > m + kRescaleThreshold) {
+    if constexpr (PACK == 3) {  // speculative: exps with the running max, the max check after
+      if (it == 0) m = mt2;
+    } else if (mt2 > m + kRescaleThreshold) {
       l *= fast_exp2(m - mt2);
       m = mt2;
     }
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) softmax_kernel(int iters, float
       else
         pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
       if constexpr (!NOSUM) acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
-      if constexpr (PACK == 0) {
+      if constexpr (PACK == 0 || PACK == 3) {
         pk[i] = pack_bf16x2(pp.x, pp.y);
       } else {  // truncate to bf16 with one byte permute (ALU pipe) instead of F2FP
         uint32_t r;
@@ -93,6 +95,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) softmax_kernel(int iters, float
     }
     const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
     l += a2.x + a2.y;
+    if constexpr (PACK == 3) {
+      if (__any_sync(0xffffffffu, mt2 > m + kRescaleThreshold)) {  // never after the first step here
+        l = 0.f;
+        m = mt2;
+      }
+    }
     // P next to S, so S stays intact for the next iteration.
     tmem_st32(scol + 64, pk);
     tmem_st_wait();
@@ -289,7 +297,7 @@ void run() {
   // One 128x64 tile = 4 warp-steps; SM throughput in tiles per cycle:
   const double sm_cycles_per_tile = per_step * 4.0 / WARPS;
   std::printf("poly %d/8 %s warps/SM=%2d (per SMSP %d): %7.1f cycles per warp-step, %7.1f SM cycles per 128x64 tile  %s\n",
-              PN, PACK == 2 ? "f16x2 ex2 " : PACK ? "prmt pack " : NOSUM ? "no row sum" : "row sum   ", WARPS, WARPS / 4, per_step, sm_cycles_per_tile,
+              PN, PACK == 3 ? "spec max  " : PACK == 2 ? "f16x2 ex2 " : PACK ? "prmt pack " : NOSUM ? "no row sum" : "row sum   ", WARPS, WARPS / 4, per_step, sm_cycles_per_tile,
               cudaGetErrorString(err));
   cudaFree(d);
   cudaFree(sink);
@@ -310,6 +318,8 @@ int main() {
   run<8, false, 2, 0>();    // ex2.approx.f16x2 (two exps per MUFU op)
   run<16, false, 2, 0>();
   run_ld<8>();
+  run<8, false, 3, 3>();   // speculative exps (running max), max check off the critical path
+  run<16, false, 3, 3>();
   run_split<16, 3>();
   run_split<16, 2>();
   run_split<8, 3>();
