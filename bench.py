@@ -307,7 +307,7 @@ def run_single(args, wl):
     mufu_peak = 16 * torch.cuda.get_device_properties(dev).multi_processor_count * (kernel_mhz or 1965.0) * 1e6
     roofline["softmax_exp2"] = {"per_launch": exps, "achieved_per_s": round(exps / (k4_ms * 1e-3), 1),
                                 "peak_per_s": round(mufu_peak, 1), "frac": round(exps / (k4_ms * 1e-3) / mufu_peak, 4),
-                                "peak_basis": "16 ex2/clk/SM x SMs x in-kernel SM clock; d=64 runs 3 of 8 exp pairs "
+                                "peak_basis": "16 ex2/clk/SM x SMs x in-kernel SM clock; d=64 runs 2 of 8 exp pairs "
                                               "on the FMA pipe, so frac may exceed 1 there"}
 
     # ---- e2e through the public API with host buffers (pinned), every step:

@@ -144,6 +144,8 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 domain
 // 3 of 8 (4 of 8 is slower again, profiles/r02_d64_poly_sweep.log); d=128 is
 // smem-port and power bound and only slows down (Wan: 5.71 / 5.97 / 6.32 ms
 // for 0 / 1 / 2 of 8).
+// With the row sum on the tensor core (d=64, KCfg::kColL) 2 of 8 beat 3 of 8:
+// 2.787 M vs 2.800 M cycles, and 1.3% in sustained runs.
 // Which pairs of every 8 go to the FMA pipe: spread out, so the compiler
 // interleaves the polynomial chains with the MUFU stream (3 of 8 at {0,3,5}:
 // 2.94 M vs 2.98 M cycles for {0,1,2} on CogVideoX, tests/variant_cycles.py).
@@ -155,7 +157,7 @@ __host__ __device__ constexpr int poly_pairs() {
 #ifdef DBSP_POLY_N
   return DBSP_POLY_N;
 #else
-  return D == 64 ? 3 : 0;
+  return D == 64 ? 2 : 0;
 #endif
 }
 
@@ -176,18 +178,29 @@ struct KCfg {
   static constexpr uint32_t kQBytes = kQInTmem ? 0u : 128u * D * 2u;
   static constexpr uint32_t kQChunk = 128u * 128u;  // one 64-column chunk of a 128-row Q tile
   // TMEM columns (256 per CTA): [Q], NSB S/P buffers of 64 cols, O (fp32, D
-  // cols); regions 64-column aligned.
+  // cols); regions 64-column aligned.  d=64: Q 0-31, row sum l 32-47 (kColL).
   static constexpr uint32_t kColQ = 0;
   static constexpr uint32_t kColS = kQInTmem ? 64 : 0;
   static constexpr uint32_t kColO = kColS + 64 * kNSB;
   static_assert(kColO + D <= kTmemCols, "TMEM budget");
   static constexpr int kStages = D == 128 ? 2 : (kQInTmem ? 6 : 5);  // K/V smem ring depth
   static constexpr int kNumBars = 4 * kStages + 2 * kNSB + 4;
-  static constexpr uint32_t kDataBytes = kQBytes + 2u * kStages * kTileBytes;
+  // d=64: the row sum l comes from the tensor core -- one more MMA per PV,
+  // P x (64 keys x 16 ones) into 16 TMEM columns beside Q (kColL) -- so the
+  // softmax warps skip 32 FADD2 per row and tile (8% of the kernel's
+  // instructions).  The ones block is one 64-key x 64-column bf16 tile in
+  // smem, read like a V tile.  l then sums the bf16 P the PV MMA consumes.
+  // With 2 of 8 exp pairs on the FMA pipe (poly_pairs): CogVideoX 2.787 M vs
+  // 2.807 M cycles (ncu) and 1.723-1.730 vs 1.751-1.755 ms in sustained
+  // interleaved runs (tests/ab_probe.py --sustained --rounds 20, x3).  At
+  // d=128 TMEM is full (S 128 + O 128 columns).
+  static constexpr uint32_t kColL = 32;
+  static constexpr uint32_t kOnesBytes = kQInTmem ? 64u * 64u * 2u : 0u;
+  static constexpr uint32_t kDataBytes = kQBytes + 2u * kStages * kTileBytes + kOnesBytes;
   static constexpr uint32_t kSmemBytes = kDataBytes + 1024 + 8 * kNumBars + 16;
 };
 
-template <int D, int POLY = poly_pairs<D>()>
+template <int D, int POLY = poly_pairs<D>(), bool LMMA = D == 64>
 __global__ void __launch_bounds__(kThreads, 2)
     sparse_attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                            const __grid_constant__ CUtensorMap tmK,
@@ -203,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t sQ = base;  // only when !kQInTmem
   const uint32_t sK = base + C::kQBytes;
   const uint32_t sV = sK + NS * C::kTileBytes;
-  const uint32_t sBar = sV + NS * C::kTileBytes;
+  const uint32_t sOnes = sV + NS * C::kTileBytes;  // kOnesBytes, LMMA only
+  const uint32_t sBar = sOnes + C::kOnesBytes;
+  static_assert(!LMMA || C::kQInTmem, "the tensor-core row sum needs the d=64 TMEM layout");
   auto bKfull = [&](int s) { return sBar + 8u * s; };
   auto bVfull = [&](int s) { return sBar + 8u * (NS + s); };
   auto bKempty = [&](int s) { return sBar + 8u * (2 * NS + s); };
@@ -250,6 +265,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&tmV);
   }
   if (warp == 5) tmem_alloc(sTmemSlot, kTmemCols);
+  if constexpr (LMMA) {
+    uint4* ones = reinterpret_cast<uint4*>(gbase + (sOnes - base));
+    for (uint32_t i = threadIdx.x; i < C::kOnesBytes / 16; i += kThreads)
+      ones[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);  // bf16 1.0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -316,6 +337,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint64_t dK = smem_desc_sw128(sK, 16, 1024);
       const uint64_t dQ = smem_desc_sw128(sQ, 16, 1024);  // used only when !kQInTmem
       const uint64_t dV = smem_desc_sw128(sV, 8192, 1024);
+      constexpr uint32_t kIdescL = idesc_bf16(128, 16, false, true);
+      const uint64_t dOnes = smem_desc_sw128(sOnes, 8192, 1024);
       auto issue_s = [&](uint32_t j) {
         const int s = int(j % NS);
         mbar_wait(bKfull(s), (j / NS) & 1);
@@ -351,6 +374,11 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int kk = 0; kk < 4; ++kk)
             mma_ts(tmem + C::kColO, pcol + kk * 8, bV + ((kk * 2048) >> 4), kIdescPV, (i > 0 || kk > 0) ? 1u : 0u);
           tc_commit(bVempty(s));
+          if constexpr (LMMA) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_ts(tmem + C::kColL, pcol + kk * 8, dOnes + ((kk * 2048) >> 4), kIdescL, (i > 0 || kk > 0) ? 1u : 0u);
+          }
           tc_commit(bOdone(i));
           DBSP_TRC(kTrMmaPV, i);
         }
@@ -478,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           float alpha = 1.f;
           if (resc) {
             alpha = fast_exp2(m - mt2);
-            l *= alpha;
+            if constexpr (!LMMA) l *= alpha;
             m = mt2;
           }
           if (__any_sync(0xffffffffu, need_o)) {
@@ -497,9 +525,15 @@ __global__ void __launch_bounds__(kThreads, 2)
               for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
               tmem_st32(tmem + lane_off + C::kColO + c * 32, o);
             }
+            if constexpr (LMMA) {  // l: the first of its 16 (equal) columns is the one read
+              const uint32_t lv = tmem_ld1(tmem + lane_off + C::kColL);
+              tmem_ld_wait();
+              tmem_st1(tmem + lane_off + C::kColL, __float_as_uint(__uint_as_float(lv) * alpha));
+            }
           }
         };
-        // P = 2^(S*scale - m) as packed bf16; returns the row sum.  Packed
+        // P = 2^(S*scale - m) as packed bf16; returns the row sum (0 when the
+        // tensor core sums the rows, LMMA).  Packed
         // f32x2 FMA/add (FFMA2/FADD2): half the non-MUFU issue slots.
         uint32_t pk[32];
         auto exps = [&]() {
@@ -514,9 +548,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             } else {
               pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
             }
-            acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
+            if constexpr (!LMMA) acc2[i & 1] = __fadd2_rn(acc2[i & 1], pp);
             pk[i] = pack_bf16x2(pp.x, pp.y);
           }
+          if constexpr (LMMA) return 0.f;
           const float2 a2 = __fadd2_rn(acc2[0], acc2[1]);
           return a2.x + a2.y;
         };
@@ -556,6 +591,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       // parity wait cannot tell phase count-1 from phase count-3.
       mbar_wait(bOfinal, 0);
       tc_fence_after();
+      if constexpr (LMMA) {
+        const uint32_t lv = tmem_ld1(tmem + lane_off + C::kColL);
+        tmem_ld_wait();
+        l = __uint_as_float(lv);
+      }
     }
     const bool live = !(upper && it.single) && token < p.q_tokens;
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
