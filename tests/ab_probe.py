@@ -1,7 +1,7 @@
 """Interleaved A/B timing of K4 schedule-flag variants on one workload: the
 B200's power cap moves the clock by +-10% between runs, so variants are timed
-round-robin (R rounds x N launches each) and compared by median of round
-medians.  GPU-box tool: python tests/ab_probe.py workload flagsA flagsB ... [--rounds R]
+round-robin (R rounds x N launches each, the order rotated every round) and
+compared by median of round medians.  GPU-box tool: python tests/ab_probe.py workload flagsA flagsB ... [--rounds R]
 (a flags entry 'F:ENV=V' sets nothing -- env is per process; use one process per env)."""
 import json
 import sys
@@ -46,8 +46,10 @@ def main():
             sc.launch(q, k, v, o)
     torch.cuda.synchronize()
     res = {f: [] for f in flag_list}
-    for _ in range(rounds):
-        for f, sc in zip(flag_list, scheds):
+    for r in range(rounds):
+        # rotate the order every round: a variant's position in the round biases it
+        rot = r % len(flag_list)
+        for f, sc in list(zip(flag_list, scheds))[rot:] + list(zip(flag_list, scheds))[:rot]:
             ts = []
             for _ in range(per_round):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
