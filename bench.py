@@ -302,7 +302,7 @@ def run_single(args, wl):
                 "kernel": lay["kernel"],
                 "timing": "CUDA events around each step's K4 launch on its stream; value (ms_per_step) "
                           "is the whole timed region / steps: every step's K2 device schedule build runs "
-                          "inside it, on a side stream overlapping the previous step's K4 (the first "
+                          "inside it, on a high-priority side stream overlapping the previous step's K4 (the first "
                           "one exposed)"}
     # Second ceiling: the softmax's exp2 on the MUFU pipe, 16 per clock per SM on B200
     # (tests/ex2h_bench.cu), at the clock measured inside the kernel.  At d=64 a 64x64
