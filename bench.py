@@ -350,9 +350,10 @@ def run_single(args, wl):
                         f"{args.e2e_chunks} head chunks (cudaMemcpy2DAsync), mask words H2D, K2 list build + K4 "
                         "per chunk on the GPU, D2H of o -- copies overlap the kernel on 3 streams"},
         "gpu_launches": n_launches,
-        "gpu_launches_note": "our kernels in the timed region (dbsp_launch_count): per step K2 "
-                             "(k2_count, k2_sorted_counts, k2_write per layout + k2_choose) and both "
-                             "gated K4 launches, one of which returns at once; CUB sort/scan not counted",
+        "gpu_launches_note": "our kernels in the timed region (dbsp_launch_count): per step the K2 "
+                             "device schedule build (k2_count, k2_plan_fused, k2_write_fused; larger "
+                             "layers take the k2_count / CUB sort / k2_sorted_counts / k2_write path, "
+                             "CUB kernels not counted) and one K4 launch",
         "clocks": {**clk.summary(), "sm_mhz_in_kernel": kernel_mhz,
                    "note": "sm_mhz: nvidia-smi samples over the timed region; sm_mhz_in_kernel: "
                            "clock64 / %globaltimer of CTA 0 inside one more K4 launch right after it"},
