@@ -527,6 +527,53 @@ def test_native_sp_context_nccl_single_rank():
     assert torch.equal(out, ref)
 
 
+@pytest.mark.parametrize("mode", ["scaled_q", "ramped_k"])
+@pytest.mark.parametrize("ring", [False, True])
+def test_d64_rescale_mid_item_row_sum_on_tensor_core(mode, ring):
+    # d=64 takes the row sum l from the tensor core (P x ones into TMEM,
+    # attn_kernel.cuh KCfg::kColL): a lazy rescale in the middle of an item
+    # must scale that l column with O, and the LSE (from l) must match; in
+    # ring mode the merged accumulators go through the same l.
+    H, S, d = 3, 2048, 64
+    nb = S // 64
+    masks = D.generate_mask_set(D.GeneratorSpec(H, nb, nb, 64, "clustered", 0.3, 0.7, 1.0, 31))
+    q, k, v = make_qkv(S, H, d, 37)
+    if mode == "scaled_q":
+        q = (q.float() * 6.0).to(torch.bfloat16)
+    else:
+        ramp = torch.linspace(0.2, 4.0, S).view(S, 1, 1)
+        q = (q.float().abs() + 0.5).to(torch.bfloat16)
+        k = (k.float().abs() * ramp + 0.1).to(torch.bfloat16)
+    ref, ref_lse = oracle.sparse_attention(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                                           masks.words, nb)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    out = torch.empty(S, H, d, device="cuda", dtype=torch.bfloat16)
+    if not ring:
+        lse = torch.empty(H, S, device="cuda", dtype=torch.float32)
+        sc = AttentionSchedule().build(masks, kv_tokens_global=S)
+        sc.launch(qd, kd, vd, out, lse=lse)
+        torch.cuda.synchronize()
+        fin = np.isfinite(ref_lse)
+        assert np.abs(lse.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+    else:
+        o_acc = torch.empty(S, H, d, dtype=torch.float32, device="cuda")
+        l_acc = torch.empty(H, S, dtype=torch.float32, device="cuda")
+        accum_init(o_acc, l_acc)
+        groups = [np.arange(0, nb, 2), np.arange(1, nb, 2)]
+        keep = []
+        for i, g in enumerate(groups):
+            kl = torch.cat([kd[b * 64:(b + 1) * 64] for b in g]).contiguous()
+            vl = torch.cat([vd[b * 64:(b + 1) * 64] for b in g]).contiguous()
+            sc = AttentionSchedule().build(masks, kv_block_ids=g, kv_tokens_global=S)
+            sc.launch(qd, kl, vl, out, o_accum=o_acc, lse_accum=l_acc, accumulate=True,
+                      finalize=(i == len(groups) - 1))
+            keep.append((sc, kl, vl))
+        torch.cuda.synchronize()
+        fin = np.isfinite(ref_lse)
+        assert np.abs(l_acc.cpu().numpy()[fin] - ref_lse[fin]).max() < 1e-2
+    check(out, ref, f"d=64 rescale {mode} ring {ring}")
+
+
 @pytest.mark.parametrize("flags", [1 | 8 | 16 | 128, 1])
 @pytest.mark.parametrize("mode", ["scaled_q", "ramped_k"])
 def test_d128_rescale_mid_item(flags, mode):
